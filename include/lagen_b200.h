@@ -1,0 +1,129 @@
+/*
+ * lagen_b200.h — C ABI of the B200 execution backend for the `lagen`
+ * blocked-variant solvers (upper Cholesky, triangular Lyapunov, triangular
+ * Sylvester) over batches of fixed-size fp64 matrices.
+ *
+ * Drop-in boundary.  The reference exposes its hot path as
+ *
+ *   (1) the emitted size-specialised C kernel
+ *         void <eq>_v<k>_n<n>_b<b>(const double* <inputs>..., double* X)
+ *       /root/reference/pkg/src/lagen/codegen.py:143-201 (signature order from
+ *       `_signature`, codegen.py:143-152; name from lowering.py:952), and
+ *   (2) the executor  interpret_algorithm(alg, inst, b)
+ *       /root/reference/pkg/src/lagen/verify.py:221-303.
+ *
+ * The batched entry points below replace both: `lagen_b200_<eq>` is (1) with
+ * the variant/n/b baked into arguments instead of the symbol name and a batch
+ * dimension added; `lagen_b200_execute` is (2) for an arbitrary synthesised
+ * statement list.  All matrices are flat row-major, ld = n, and a batch is
+ * `batch` contiguous n*n problems (stride n*n doubles).  Inputs follow the
+ * reference's `_signature` order (inputs in declaration order, then X).
+ *
+ * Differences to the reference contract (supersets):
+ *   - X need not be zero-initialised: every one of the n*n entries is written
+ *     (zeros below the diagonal for Cholesky, the mirror for Lyapunov).
+ *   - Errors are reported, not silent: `info[p]` (optional, may be NULL) is
+ *     0 on success, i+1 if the Cholesky leaf met a non-positive pivot at
+ *     global index i (kernels.py:87-88), and -1 if X holds NaN/Inf
+ *     (verify.py:301-302).
+ *   - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream).  Device pointers unless stated otherwise.
+ *   - Return value: LAGEN_OK or a negative LAGEN_E* code; no C++ exception
+ *     crosses the ABI; lagen_b200_last_error() gives a thread-local message.
+ */
+#ifndef LAGEN_B200_H
+#define LAGEN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LAGEN_B200_ABI_VERSION 1
+#define LAGEN_MAX_STMTS 16
+
+/* equations (the three shipped cases, /root/reference/pkg/cases/ *.la) */
+enum {
+  LAGEN_CHOLESKY = 0,  /* X^T X = A,        inputs (A)       */
+  LAGEN_LYAPUNOV = 1,  /* L X + X L^T = S,  inputs (L, S)    */
+  LAGEN_SYLVESTER = 2  /* L X + X U = C,    inputs (L, U, C) */
+};
+
+/* statement kinds (worksheet.py:47-67, dispatch at verify.py:263-295) */
+enum {
+  LAGEN_GEMM_UPDATE = 0,
+  LAGEN_CHOL = 1,
+  LAGEN_TRSM_LEFT_TRANSPOSED = 2,
+  LAGEN_SYLV = 3,
+  LAGEN_LYAP = 4
+};
+
+/* operand codes inside a statement: 0 = the unknown's storage X, then the
+ * coefficient operands in declaration order (L = 1, U = 2); -1 = unused. */
+typedef struct lagen_view {
+  int8_t op, r, c, trans;  /* 3x3 repartition block (r, c) of `op`, maybe ^T (worksheet.py:29-44) */
+} lagen_view;
+
+typedef struct lagen_stmt {
+  int8_t kind;             /* LAGEN_GEMM_UPDATE ... */
+  int8_t sign;             /* +1 / -1 (GEMM_update sign) */
+  lagen_view out;          /* written in place, never transposed */
+  lagen_view in[2];        /* read views (coefficients / factors) */
+} lagen_stmt;
+
+/* status codes */
+#define LAGEN_OK 0
+#define LAGEN_EINVAL (-1)       /* null pointer, negative batch, bad equation */
+#define LAGEN_EUNSUPPORTED (-2) /* (n, b) has no sm_100a instantiation or b does not divide n */
+#define LAGEN_EVARIANT (-3)     /* statement list malformed / unknown variant index */
+#define LAGEN_ECUDA (-4)        /* CUDA runtime error (launch, copy, allocation) */
+
+int lagen_b200_abi_version(void);
+const char* lagen_b200_last_error(void);
+
+/* ---- variant table (enumerate_algorithms() output, worksheet.py:281) ---- */
+int lagen_b200_num_variants(int eq);
+/* copies the statement list of `variant` into out[0..cap); returns the count or <0 */
+int lagen_b200_variant_stmts(int eq, int variant, lagen_stmt* out, int cap);
+/* 1 if a kernel is instantiated for (eq, n, b), else 0 */
+int lagen_b200_supported(int eq, int n, int b);
+/* launch geometry chosen for (eq, n, b): threads per problem, problems per CTA,
+ * threads per CTA, dynamic shared memory bytes; returns 0 or <0 */
+int lagen_b200_geometry(int eq, int n, int b, int* threads_per_problem,
+                        int* problems_per_cta, int* threads_per_cta, int* smem_bytes);
+
+/* ---- batched solvers: the emitted kernel <eq>_v<k>_n<n>_b<b> of codegen.py:155-201 ---- */
+int lagen_b200_cholesky(int variant, int n, int b, long long batch,
+                        const double* A, double* X, int* info, void* stream);
+int lagen_b200_lyapunov(int variant, int n, int b, long long batch,
+                        const double* L, const double* S, double* X, int* info,
+                        void* stream);
+int lagen_b200_sylvester(int variant, int n, int b, long long batch,
+                         const double* L, const double* U, const double* C,
+                         double* X, int* info, void* stream);
+
+/* ---- generic executor: interpret_algorithm(alg, inst, b), verify.py:221 ----
+ * inputs[] in _signature order: chol {A}, lyap {L, S}, sylv {L, U, C}. */
+int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
+                       long long batch, const double* const* inputs, double* X,
+                       int* info, void* stream);
+
+/* Same, but every buffer is in HOST memory (pinned for full overlap).  The
+ * batch is streamed through the device in chunks, H2D copy / solve / D2H copy
+ * pipelined over two streams; synchronous on return. */
+int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
+                            long long batch, const double* const* h_inputs,
+                            double* h_X, int* h_info);
+
+/* ---- seeded batched generator (BASELINE.json configs) ----
+ * Writes problems [first, first + batch) of the seeded stream into outputs[]
+ * (device, _signature order).  Problem p depends only on (eq, n, seed, p), so
+ * any sharding of the index range sees identical problems. */
+int lagen_b200_generate(int eq, int n, unsigned long long seed, long long first,
+                        long long batch, double* const* outputs, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAGEN_B200_H */

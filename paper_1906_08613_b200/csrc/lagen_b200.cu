@@ -1,0 +1,269 @@
+// lagen_b200.cu — the C ABI (include/lagen_b200.h): validation, (eq, n, b)
+// dispatch to the size-specialised instances, the host-buffer pipeline and
+// the seeded batched generator.  No C++ exception crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "inst_index.h"
+#include "lagen_b200.h"
+#include "registry.cuh"
+#include "variants_table.h"
+
+using namespace lagen;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(LAGEN_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+const KernelEntry* find_entry(int eq, int n, int b) {
+  if (eq < 0 || eq > 2) return nullptr;
+  for (int p = 0; p < kTableParts; ++p) {
+    const EntryTable& t = kTables[eq][p];
+    for (int i = 0; i < *t.n; ++i)
+      if (t.e[i].n == n && t.e[i].b == b) return &t.e[i];
+  }
+  return nullptr;
+}
+
+int eq_ninputs(int eq) { return eq + 1; }
+int eq_ncoef(int eq) { return eq; }  // chol 0, lyap 1 (L), sylv 2 (L, U)
+
+// Structural checks mirroring verify.py:263-295 / worksheet.py:47-67.
+int validate(int eq, const lagen_stmt* stmts, int nstmts) {
+  if (!stmts || nstmts <= 0) return fail(LAGEN_EVARIANT, "empty statement list");
+  if (nstmts > LAGEN_MAX_STMTS) return fail(LAGEN_EVARIANT, "more than LAGEN_MAX_STMTS statements");
+  static const int arity[5] = {2, 0, 1, 2, 1};
+  const int ncoef = eq_ncoef(eq);
+  for (int s = 0; s < nstmts; ++s) {
+    const lagen_stmt& S = stmts[s];
+    if (S.kind < 0 || S.kind > 4) return fail(LAGEN_EVARIANT, "unknown statement kind");
+    if (S.out.op != 0) return fail(LAGEN_EVARIANT, "statement writes outside the output");
+    if (S.out.trans) return fail(LAGEN_EVARIANT, "transposed output view");
+    if (S.out.r < 0 || S.out.r > 2 || S.out.c < 0 || S.out.c > 2)
+      return fail(LAGEN_EVARIANT, "block index out of range");
+    if (S.kind == LAGEN_CHOL && (eq != LAGEN_CHOLESKY || S.out.r != S.out.c))
+      return fail(LAGEN_EVARIANT, "CHOL statement outside a Cholesky diagonal block");
+    if (S.kind == LAGEN_LYAP && (eq != LAGEN_LYAPUNOV || S.out.r != S.out.c))
+      return fail(LAGEN_EVARIANT, "LYAP statement outside a Lyapunov diagonal block");
+    if (S.kind == LAGEN_SYLV && eq == LAGEN_CHOLESKY) return fail(LAGEN_EVARIANT, "SYLV in Cholesky");
+    if (S.kind == LAGEN_GEMM_UPDATE && S.sign != 1 && S.sign != -1)
+      return fail(LAGEN_EVARIANT, "GEMM sign must be +-1");
+    for (int j = 0; j < 2; ++j) {
+      const lagen_view& v = S.in[j];
+      if (j < arity[S.kind]) {
+        if (v.op < 0 || v.op > ncoef) return fail(LAGEN_EVARIANT, "input view operand out of range");
+        if (v.r < 0 || v.r > 2 || v.c < 0 || v.c > 2) return fail(LAGEN_EVARIANT, "input block out of range");
+        if (v.trans != 0 && v.trans != 1) return fail(LAGEN_EVARIANT, "bad transpose flag");
+        // coefficient diagonal blocks are packed (diag in a pad column): GEMM
+        // operands from L/U must be off-diagonal blocks (true for every
+        // synthesised variant)
+        if (S.kind == LAGEN_GEMM_UPDATE && v.op > 0 && v.r == v.c)
+          return fail(LAGEN_EVARIANT, "GEMM operand is a diagonal block of a triangular coefficient");
+        if ((S.kind == LAGEN_SYLV || S.kind == LAGEN_LYAP || S.kind == LAGEN_TRSM_LEFT_TRANSPOSED) &&
+            v.r != v.c)
+          return fail(LAGEN_EVARIANT, "triangular coefficient is not a diagonal block");
+      } else if (v.op != -1) {
+        return fail(LAGEN_EVARIANT, "unexpected input view");
+      }
+    }
+    if (S.kind == LAGEN_TRSM_LEFT_TRANSPOSED) {
+      // logically lower coefficient: X^T of the upper factor (kernels.py:47-60)
+      const lagen_view& v = S.in[0];
+      const bool lower = (v.op == 0) ? (v.trans == 1) : (v.op == 1 ? v.trans == 0 : v.trans == 1);
+      if (eq != LAGEN_CHOLESKY || !lower)
+        return fail(LAGEN_EVARIANT, "TRSM coefficient must be logically lower");
+    }
+  }
+  return LAGEN_OK;
+}
+
+int check_common(int eq, int n, int b, long long batch) {
+  if (eq < 0 || eq > 2) return fail(LAGEN_EINVAL, "unknown equation");
+  if (batch < 0) return fail(LAGEN_EINVAL, "negative batch");
+  if (n < 1 || b < 1 || n % b) return fail(LAGEN_EUNSUPPORTED, "block size does not divide n");
+  if (!find_entry(eq, n, b))
+    return fail(LAGEN_EUNSUPPORTED, "no sm_100a instance for (n=" + std::to_string(n) + ", b=" +
+                                        std::to_string(b) + ")");
+  return LAGEN_OK;
+}
+
+const lagen_stmt* builtin(int eq, int variant, int* count) {
+  switch (eq) {
+    case LAGEN_CHOLESKY:
+      if (variant < 0 || variant >= kNumVariants_cholesky) return nullptr;
+      *count = kNumStmts_cholesky[variant];
+      return kStmts_cholesky[variant];
+    case LAGEN_LYAPUNOV:
+      if (variant < 0 || variant >= kNumVariants_lyapunov) return nullptr;
+      *count = kNumStmts_lyapunov[variant];
+      return kStmts_lyapunov[variant];
+    case LAGEN_SYLVESTER:
+      if (variant < 0 || variant >= kNumVariants_sylvester) return nullptr;
+      *count = kNumStmts_sylvester[variant];
+      return kStmts_sylvester[variant];
+  }
+  return nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lagen_b200_abi_version(void) { return LAGEN_B200_ABI_VERSION; }
+
+const char* lagen_b200_last_error(void) { return g_last_error.c_str(); }
+
+int lagen_b200_num_variants(int eq) {
+  switch (eq) {
+    case LAGEN_CHOLESKY: return kNumVariants_cholesky;
+    case LAGEN_LYAPUNOV: return kNumVariants_lyapunov;
+    case LAGEN_SYLVESTER: return kNumVariants_sylvester;
+  }
+  return fail(LAGEN_EINVAL, "unknown equation");
+}
+
+int lagen_b200_variant_stmts(int eq, int variant, lagen_stmt* out, int cap) {
+  int count = 0;
+  const lagen_stmt* s = builtin(eq, variant, &count);
+  if (!s) return fail(LAGEN_EVARIANT, "unknown variant index");
+  if (out) {
+    if (cap < count) return fail(LAGEN_EINVAL, "output capacity too small");
+    std::memcpy(out, s, sizeof(lagen_stmt) * count);
+  }
+  return count;
+}
+
+int lagen_b200_supported(int eq, int n, int b) { return find_entry(eq, n, b) ? 1 : 0; }
+
+int lagen_b200_geometry(int eq, int n, int b, int* g, int* p, int* threads, int* smem) {
+  const KernelEntry* e = find_entry(eq, n, b);
+  if (!e) return fail(LAGEN_EUNSUPPORTED, "no instance");
+  if (g) *g = e->G;
+  if (p) *p = e->P;
+  if (threads) *threads = e->threads;
+  if (smem) *smem = e->smem;
+  return LAGEN_OK;
+}
+
+int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
+                       const double* const* inputs, double* X, int* info, void* stream) {
+  int rc = check_common(eq, n, b, batch);
+  if (rc) return rc;
+  rc = validate(eq, stmts, nstmts);
+  if (rc) return rc;
+  if (batch == 0) return LAGEN_OK;
+  if (!inputs || !X) return fail(LAGEN_EINVAL, "null buffer");
+  for (int i = 0; i < eq_ninputs(eq); ++i)
+    if (!inputs[i]) return fail(LAGEN_EINVAL, "null input buffer");
+  LaunchArgs a;
+  std::memset(&a, 0, sizeof(a));
+  std::memcpy(a.sl.s, stmts, sizeof(lagen_stmt) * nstmts);
+  a.sl.count = nstmts;
+  for (int i = 0; i < 3; ++i) a.in[i] = i < eq_ninputs(eq) ? inputs[i] : inputs[0];
+  a.X = X;
+  a.info = info;
+  a.batch = batch;
+  const KernelEntry* e = find_entry(eq, n, b);
+  cudaError_t err = e->launch(a, static_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "solve launch");
+  return LAGEN_OK;
+}
+
+static int run_variant(int eq, int variant, int n, int b, long long batch, const double* const* in, double* X,
+                       int* info, void* stream) {
+  int count = 0;
+  const lagen_stmt* s = builtin(eq, variant, &count);
+  if (!s) return fail(LAGEN_EVARIANT, "unknown variant index");
+  return lagen_b200_execute(eq, s, count, n, b, batch, in, X, info, stream);
+}
+
+int lagen_b200_cholesky(int variant, int n, int b, long long batch, const double* A, double* X, int* info,
+                        void* stream) {
+  const double* in[1] = {A};
+  return run_variant(LAGEN_CHOLESKY, variant, n, b, batch, in, X, info, stream);
+}
+
+int lagen_b200_lyapunov(int variant, int n, int b, long long batch, const double* L, const double* S, double* X,
+                        int* info, void* stream) {
+  const double* in[2] = {L, S};
+  return run_variant(LAGEN_LYAPUNOV, variant, n, b, batch, in, X, info, stream);
+}
+
+int lagen_b200_sylvester(int variant, int n, int b, long long batch, const double* L, const double* U,
+                         const double* C, double* X, int* info, void* stream) {
+  const double* in[3] = {L, U, C};
+  return run_variant(LAGEN_SYLVESTER, variant, n, b, batch, in, X, info, stream);
+}
+
+// Host-buffer pipeline: chunks of the batch cycle through two device
+// buffer sets on two streams so H2D(c+1), solve(c) and D2H(c-1) overlap.
+int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
+                            const double* const* h_inputs, double* h_X, int* h_info) {
+  int rc = check_common(eq, n, b, batch);
+  if (rc) return rc;
+  rc = validate(eq, stmts, nstmts);
+  if (rc) return rc;
+  if (batch == 0) return LAGEN_OK;
+  if (!h_inputs || !h_X) return fail(LAGEN_EINVAL, "null buffer");
+  const int nin = eq_ninputs(eq);
+  for (int i = 0; i < nin; ++i)
+    if (!h_inputs[i]) return fail(LAGEN_EINVAL, "null input buffer");
+  const size_t prob_bytes = sizeof(double) * (size_t)n * n;
+  // ~32 MiB of input per chunk and operand, at least one problem
+  long long chunk = (32ll << 20) / (long long)prob_bytes;
+  if (chunk < 1) chunk = 1;
+  if (chunk > batch) chunk = batch;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  double* d_in[2][3] = {{nullptr}};
+  double* d_X[2] = {nullptr, nullptr};
+  int* d_info[2] = {nullptr, nullptr};
+  cudaError_t err = cudaSuccess;
+  for (int k = 0; k < 2 && err == cudaSuccess; ++k) {
+    err = cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
+    for (int i = 0; i < nin && err == cudaSuccess; ++i) err = cudaMallocAsync(&d_in[k][i], chunk * prob_bytes, st[k]);
+    if (err == cudaSuccess) err = cudaMallocAsync(&d_X[k], chunk * prob_bytes, st[k]);
+    if (err == cudaSuccess && h_info) err = cudaMallocAsync(&d_info[k], chunk * sizeof(int), st[k]);
+  }
+  int status = LAGEN_OK;
+  if (err != cudaSuccess) status = cuda_fail(err, "host pipeline setup");
+  for (long long c0 = 0, it = 0; status == LAGEN_OK && c0 < batch; c0 += chunk, ++it) {
+    const int k = (int)(it & 1);
+    const long long cnt = (batch - c0) < chunk ? (batch - c0) : chunk;
+    for (int i = 0; i < nin && err == cudaSuccess; ++i)
+      err = cudaMemcpyAsync(d_in[k][i], h_inputs[i] + c0 * n * n, cnt * prob_bytes, cudaMemcpyHostToDevice, st[k]);
+    if (err != cudaSuccess) { status = cuda_fail(err, "H2D"); break; }
+    const double* ins[3] = {d_in[k][0], d_in[k][1], d_in[k][2]};
+    status = lagen_b200_execute(eq, stmts, nstmts, n, b, cnt, ins, d_X[k], d_info[k], st[k]);
+    if (status != LAGEN_OK) break;
+    err = cudaMemcpyAsync(h_X + c0 * n * n, d_X[k], cnt * prob_bytes, cudaMemcpyDeviceToHost, st[k]);
+    if (err == cudaSuccess && h_info)
+      err = cudaMemcpyAsync(h_info + c0, d_info[k], cnt * sizeof(int), cudaMemcpyDeviceToHost, st[k]);
+    if (err != cudaSuccess) { status = cuda_fail(err, "D2H"); break; }
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (!st[k]) continue;
+    for (int i = 0; i < 3; ++i)
+      if (d_in[k][i]) cudaFreeAsync(d_in[k][i], st[k]);
+    if (d_X[k]) cudaFreeAsync(d_X[k], st[k]);
+    if (d_info[k]) cudaFreeAsync(d_info[k], st[k]);
+    cudaError_t e2 = cudaStreamSynchronize(st[k]);
+    if (e2 != cudaSuccess && status == LAGEN_OK) status = cuda_fail(e2, "host pipeline sync");
+    cudaStreamDestroy(st[k]);
+  }
+  return status;
+}
+
+}  // extern "C"

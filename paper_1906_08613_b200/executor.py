@@ -1,0 +1,212 @@
+"""Host-side executor API: the reference's hot-path interface backed by the
+sm_100a kernels.
+
+Reference interface being replaced:
+  * interpret_algorithm(alg, inst, b, on_iteration=None) -> ({X: ndarray}, flops)
+      /root/reference/pkg/src/lagen/verify.py:221-303
+  * the emitted kernel <eq>_v<k>_n<n>_b<b>(inputs..., X)
+      /root/reference/pkg/src/lagen/codegen.py:155-201
+Batched additions:
+  * solve(eq, inputs, variant=..., b=...) on [batch, n, n] fp64 CUDA tensors
+  * execute_batched(alg, n, b, {name: tensor}) -> {X: tensor}
+  * solve_host(...) for host (numpy / pinned) buffers through the pipelined
+    C entry point
+  * generate(eq, n, seed, batch, first) — the seeded batched generator.
+
+Everything runs on the GPU through liblagen_b200.so; there is no CPU path.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib, dispatch, errors
+from .variants import (EQ_CODES, EQ_INPUTS, EQUATIONS, Variant, builtin_variants,
+                       classify_equation, encode_algorithm, flop_count, validate)
+
+
+def _eq_name(eq):
+    if isinstance(eq, str):
+        if eq not in EQUATIONS:
+            # accept the reference's short names (verify.classify)
+            short = {"chol": "cholesky", "lyap": "lyapunov", "sylv": "sylvester"}
+            if eq in short:
+                return short[eq]
+            raise errors.UsageError(f"unknown equation {eq!r}")
+        return eq
+    if isinstance(eq, int):
+        return EQUATIONS[eq]
+    return classify_equation(eq)
+
+
+def resolve_variant(eq_name, variant):
+    """variant: None (dispatch), int index, Variant, reference Algorithm, or a
+    list of encoded statement dicts.  Returns (stmts, variant_index_or_None)."""
+    if variant is None:
+        return None, None
+    if isinstance(variant, int):
+        vs = builtin_variants(eq_name)
+        if not 0 <= variant < len(vs):
+            raise errors.VariantError(f"{eq_name} has {len(vs)} variants, not {variant}")
+        return vs[variant].statements, variant
+    if isinstance(variant, Variant):
+        return variant.statements, variant.index
+    if hasattr(variant, "statements") and hasattr(variant, "equation"):
+        return encode_algorithm(variant), getattr(variant, "index", None)
+    return list(variant), None
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check_inputs(eq_name, inputs, n=None):
+    names = EQ_INPUTS[eq_name]
+    if len(inputs) != len(names):
+        raise errors.UsageError(f"{eq_name} takes inputs {names}, got {len(inputs)} tensors")
+    shape = None
+    for nm, t in zip(names, inputs):
+        if not isinstance(t, torch.Tensor):
+            raise errors.UsageError(f"input {nm} must be a torch.Tensor")
+        if t.dtype != torch.float64:
+            raise errors.UsageError(f"input {nm} must be float64, got {t.dtype}")
+        if not t.is_cuda:
+            raise errors.UsageError(f"input {nm} must live on a CUDA device")
+        if t.dim() != 3 or t.shape[1] != t.shape[2]:
+            raise errors.UsageError(f"input {nm} must be [batch, n, n], got {tuple(t.shape)}")
+        if not t.is_contiguous():
+            raise errors.UsageError(f"input {nm} must be contiguous (row-major, ld = n)")
+        if shape is None:
+            shape = tuple(t.shape)
+        elif tuple(t.shape) != shape:
+            raise errors.UsageError("inputs disagree in shape")
+    if n is not None and shape[1] != n:
+        raise errors.UsageError(f"inputs are {shape[1]}x{shape[1]}, expected n={n}")
+    return shape[0], shape[1]
+
+
+def solve(eq, inputs, variant=None, b=None, out=None, info=None, stream=None, check=True):
+    """Solve a batch: inputs in _signature order (chol: A; lyap: L, S;
+    sylv: L, U, C), each [batch, n, n] float64 CUDA contiguous.
+
+    variant/b default to the dispatch table (the GPU analogue of cli._select).
+    Returns (X, info).  With check=True a non-zero info raises
+    VerificationError like the reference (kernels.py:87-88, verify.py:301-302);
+    that forces a device sync."""
+    eq_name = _eq_name(eq)
+    batch, n = _check_inputs(eq_name, inputs)
+    stmts, _ = resolve_variant(eq_name, variant)
+    if stmts is None:
+        pick = dispatch.select(eq_name, n)
+        stmts = builtin_variants(eq_name)[pick["variant"]].statements
+        b = b or pick["b"]
+    if b is None:
+        b = dispatch.select(eq_name, n)["b"]
+    validate(eq_name, stmts)
+    dev = inputs[0].device
+    if out is None:
+        out = torch.empty((batch, n, n), dtype=torch.float64, device=dev)
+    if info is None:
+        info = torch.empty(batch, dtype=torch.int32, device=dev)
+    arr = _lib.stmt_array(stmts)
+    ptrs = (ctypes.c_void_p * 3)(*([t.data_ptr() for t in inputs] + [0] * (3 - len(inputs))))
+    with torch.cuda.device(dev):
+        rc = _lib.lib.lagen_b200_execute(EQ_CODES[eq_name], ctypes.addressof(arr), len(stmts), n, b,
+                                         batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
+                                         ctypes.c_void_p(info.data_ptr()), _stream_ptr(stream))
+    _lib.check(rc, f"{eq_name} n={n} b={b}")
+    if check and batch:
+        bad = torch.nonzero(info).flatten()
+        if bad.numel():
+            p = int(bad[0])
+            code = int(info[p])
+            if code > 0:
+                raise errors.VerificationError(f"problem {p}: non-positive pivot at index {code - 1}")
+            raise errors.VerificationError(f"problem {p}: NaN or Inf produced: ill-posed instance or bug")
+    return out, info
+
+
+def execute_batched(alg, n, b, inputs, stream=None, check=True):
+    """SURVEY §8b Python side: semantics of interpret_algorithm over a batch.
+
+    alg: reference Algorithm, Variant, or (eq_name, variant_index);
+    inputs: {operand name: [batch, n, n] CUDA tensor}.  Returns {X: tensor}."""
+    if isinstance(alg, tuple):
+        eq_name, alg = alg
+    elif isinstance(alg, Variant):
+        eq_name = alg.equation
+    else:
+        eq_name = _eq_name(alg.equation)
+    tensors = [inputs[nm] for nm in EQ_INPUTS[eq_name]]
+    X, _ = solve(eq_name, tensors, variant=alg, b=b, stream=stream, check=check)
+    _check_inputs(eq_name, tensors, n)
+    return {"X": X}
+
+
+def interpret_algorithm(alg, inst, b, on_iteration=None):
+    """Drop-in for verify.interpret_algorithm (verify.py:221-303) on one
+    reference Instance, executed by the CUDA kernel.  Returns
+    ({X: ndarray}, flops) with flops from the reference's exact model."""
+    if on_iteration is not None:
+        raise errors.UsageError("on_iteration hooks need the per-iteration interpreter; "
+                                "the fused CUDA kernel has no iteration boundary")
+    eq_name = _eq_name(alg.equation)
+    n = inst.n
+    if n % b:
+        raise errors.VerificationError(f"block size {b} does not divide {n}")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    tensors = [torch.from_numpy(np.ascontiguousarray(inst.bindings[nm], dtype=np.float64))
+               .reshape(1, n, n).to(dev) for nm in EQ_INPUTS[eq_name]]
+    X, _ = solve(eq_name, tensors, variant=alg, b=b)
+    stmts, _ = resolve_variant(eq_name, alg)
+    return {alg.output: X[0].cpu().numpy()}, flop_count(eq_name, stmts, n, b)
+
+
+def solve_host(eq, inputs, variant=None, b=None, out=None, info=None):
+    """Host buffers (numpy arrays or CPU tensors, ideally pinned) -> host X.
+    Streams the batch through the GPU with H2D / solve / D2H overlap."""
+    eq_name = _eq_name(eq)
+    arrs = []
+    for t in inputs:
+        if isinstance(t, torch.Tensor):
+            if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+                raise errors.UsageError("host inputs must be contiguous float64 CPU tensors")
+            arrs.append(t)
+        else:
+            a = np.ascontiguousarray(t, dtype=np.float64)
+            arrs.append(torch.from_numpy(a))
+    batch, n = arrs[0].shape[0], arrs[0].shape[1]
+    stmts, _ = resolve_variant(eq_name, variant)
+    if stmts is None:
+        pick = dispatch.select(eq_name, n)
+        stmts = builtin_variants(eq_name)[pick["variant"]].statements
+        b = b or pick["b"]
+    validate(eq_name, stmts)
+    if out is None:
+        out = torch.empty((batch, n, n), dtype=torch.float64, pin_memory=arrs[0].is_pinned())
+    if info is None:
+        info = torch.empty(batch, dtype=torch.int32)
+    arr = _lib.stmt_array(stmts)
+    ptrs = (ctypes.c_void_p * 3)(*([t.data_ptr() for t in arrs] + [0] * (3 - len(arrs))))
+    rc = _lib.lib.lagen_b200_execute_host(EQ_CODES[eq_name], ctypes.addressof(arr), len(stmts), n, b,
+                                          batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
+                                          ctypes.c_void_p(info.data_ptr()))
+    _lib.check(rc, f"{eq_name} host n={n} b={b}")
+    return out, info
+
+
+def generate(eq, n, seed, batch, first=0, device=None, stream=None):
+    """Seeded batched inputs (BASELINE.json distributions) for problems
+    [first, first + batch); returns tensors in _signature order."""
+    eq_name = _eq_name(eq)
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    outs = [torch.empty((batch, n, n), dtype=torch.float64, device=dev) for _ in EQ_INPUTS[eq_name]]
+    ptrs = (ctypes.c_void_p * 3)(*([t.data_ptr() for t in outs] + [0] * (3 - len(outs))))
+    with torch.cuda.device(dev):
+        rc = _lib.lib.lagen_b200_generate(EQ_CODES[eq_name], n, seed, first, batch,
+                                          ctypes.addressof(ptrs), _stream_ptr(stream))
+    _lib.check(rc, "generate")
+    return outs

@@ -1,0 +1,100 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/lagen_b200.h declares, carries the reference's variant table,
+and rejects malformed calls before touching the device."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_1906_08613_b200 import _lib
+from paper_1906_08613_b200.variants import EQ_CODES, EQUATIONS, builtin_variants, default_blocks
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "lagen_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(lagen_b200_\w+)\s*\(", text)))
+
+
+def test_header_declares_what_python_binds():
+    assert set(declared_symbols()) == set(_lib.EXPORTED)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    for sym in declared_symbols():
+        assert hasattr(lib, sym), sym
+
+
+def test_abi_version():
+    assert _lib.lib.lagen_b200_abi_version() == 1
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+def test_variant_table_matches_reference_enumeration(eq):
+    lib = _lib.lib
+    vs = builtin_variants(eq)
+    assert lib.lagen_b200_num_variants(EQ_CODES[eq]) == len(vs)
+    for v in vs:
+        arr = (_lib.Stmt * 16)()
+        cnt = lib.lagen_b200_variant_stmts(EQ_CODES[eq], v.index, ctypes.addressof(arr), 16)
+        assert cnt == len(v.statements)
+        for k, s in enumerate(v.statements):
+            got = arr[k]
+            assert (got.kind, got.sign) == (s["kind"], s["sign"])
+            assert (got.out.op, got.out.r, got.out.c) == tuple(s["out"])
+            for j in range(2):
+                gv = got.ins[j]
+                assert (gv.op, gv.r, gv.c, gv.trans) == tuple(s["ins"][j])
+    assert lib.lagen_b200_variant_stmts(EQ_CODES[eq], len(vs), None, 0) == -3
+
+
+def test_every_size_and_default_block_is_instantiated():
+    lib = _lib.lib
+    for eq in range(3):
+        for n in range(4, 129, 4):
+            for b in default_blocks(n):
+                assert lib.lagen_b200_supported(eq, n, b) == 1, (eq, n, b)
+            assert lib.lagen_b200_supported(eq, n, 3) == 0
+        assert lib.lagen_b200_supported(eq, 132, 4) == 0
+
+
+def test_geometry_fits_the_sm():
+    for eq in range(3):
+        for n in range(4, 129, 4):
+            for b in default_blocks(n):
+                g = _lib.geometry(eq, n, b)
+                assert g["threads_per_cta"] <= 1024
+                assert g["smem_bytes"] <= 227 * 1024
+                assert g["threads_per_cta"] == g["threads_per_problem"] * g["problems_per_cta"]
+
+
+def _execute(eq, stmts, n, b, batch, inputs=None, X=None):
+    arr = _lib.stmt_array(stmts) if stmts else None
+    ptrs = inputs
+    return _lib.lib.lagen_b200_execute(eq, ctypes.addressof(arr) if arr is not None else None,
+                                       len(stmts) if stmts else 0, n, b, batch,
+                                       ctypes.addressof(ptrs) if ptrs is not None else None, X, None, None)
+
+
+def test_rejects_bad_arguments_without_a_device():
+    v = builtin_variants("cholesky")[2].statements
+    assert _execute(0, v, 16, 4, -1) == -1            # negative batch
+    assert _execute(7, v, 16, 4, 1) == -1             # unknown equation
+    assert _execute(0, v, 18, 4, 1) == -2             # b does not divide n
+    assert _execute(0, v, 132, 4, 1) == -2            # no instance
+    assert _execute(0, [], 16, 4, 1) == -3            # empty statement list
+    bad = [dict(s) for s in v]
+    bad[0] = dict(bad[0], kind=9)
+    assert _execute(0, bad, 16, 4, 1) == -3           # unknown kind
+    bad = [dict(s) for s in v]
+    bad[2] = dict(bad[2], out=(1, 2, 2))
+    assert _execute(0, bad, 16, 4, 1) == -3           # writes outside the output
+    assert _execute(0, v, 16, 4, 1) == -1             # null buffers
+    assert b"null" in _lib.lib.lagen_b200_last_error()
+    assert _execute(0, v, 16, 4, 0) == 0              # empty batch is a no-op
+    lyap = builtin_variants("lyapunov")[0].statements
+    assert _execute(0, lyap, 16, 4, 1) == -3          # LYAP/SYLV inside Cholesky

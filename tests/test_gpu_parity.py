@@ -1,0 +1,234 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference.
+
+  * golden vectors of the reference's interpret_algorithm, every variant,
+    every default b, n in {4, 8, 12, 16, 24, 32}, two instance families;
+  * the CPU oracle (oracle/lagen_oracle.c, pinned to the reference by
+    test_oracle_golden.py) on device-generated BASELINE inputs, every
+    variant x b at every n in 4..128;
+  * size-independent properties at full BASELINE batch sizes (residual,
+    exact structure, shard invariance, host pipeline == device path).
+
+Tolerances (BASELINE.json north_star): per-problem relative Frobenius
+difference <= 1e-10 and residual ||op(X) - RHS||_F / ||RHS||_F <= 10 n eps.
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_1906_08613_b200 import errors, executor  # noqa: E402
+from paper_1906_08613_b200.variants import (EQ_INPUTS, EQUATIONS, builtin_variants,  # noqa: E402
+                                             default_blocks)
+
+EPS = np.finfo(np.float64).eps
+REL_TOL = 1e-10
+GOLDEN = Path(__file__).resolve().parent / "golden"
+META = json.loads((GOLDEN / "golden_meta.json").read_text())
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    torch.cuda.set_device(0)
+
+
+def rel_diff(X, Y):
+    num = np.linalg.norm((X - Y).reshape(X.shape[0], -1), axis=1)
+    den = np.maximum(1.0, np.linalg.norm(Y.reshape(Y.shape[0], -1), axis=1))
+    return num / den
+
+
+def to_dev(arrs):
+    return [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in arrs]
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+def test_golden_reference_vectors(eq):
+    d = np.load(GOLDEN / f"{eq}.npz")
+    vs = builtin_variants(eq)
+    worst = 0.0
+    groups = {}
+    for e in META[eq]["entries"]:
+        groups.setdefault((e["n"], e["variant"], e["b"]), []).append(e)
+    for (n, v, b), es in groups.items():
+        ins = [np.stack([d[f"in_{e['case']}_{n}_{nm}"] for e in es]) for nm in EQ_INPUTS[eq]]
+        X, info = executor.solve(eq, to_dev(ins), variant=v, b=b)
+        X = X.cpu().numpy()
+        want = np.stack([d[e["key"]] for e in es])
+        assert (info.cpu().numpy() == 0).all()
+        err = rel_diff(X, want).max()
+        worst = max(worst, err)
+        assert err <= REL_TOL, (eq, n, v, b, err)
+        if eq == "cholesky":
+            assert np.all(np.tril(X, -1) == 0.0)
+        if eq == "lyapunov":
+            assert np.array_equal(X, np.transpose(X, (0, 2, 1)))
+    print(f"{eq}: worst relative difference vs reference interpreter {worst:.3e}")
+
+
+SWEEP_N = list(range(4, 129, 4))
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+@pytest.mark.parametrize("n", SWEEP_N)
+def test_every_variant_vs_oracle(eq, n, oracle_mod):
+    batch = 48 if n <= 64 else 24
+    ins_d = executor.generate(eq, n, seed=n, batch=batch)
+    ins_h = [t.cpu().numpy() for t in ins_d]
+    vs = builtin_variants(eq)
+    ref_X, ref_info = oracle_mod.execute(eq, vs[0].statements, n, default_blocks(n)[0], ins_h)
+    assert (ref_info == 0).all()
+    res_tol = 10 * n * EPS
+    for v in vs:
+        for b in default_blocks(n):
+            X, info = executor.solve(eq, ins_d, variant=v.index, b=b)
+            X = X.cpu().numpy()
+            assert (info.cpu().numpy() == 0).all()
+            err = rel_diff(X, ref_X).max()
+            assert err <= REL_TOL, (eq, n, v.index, b, err)
+            res = oracle_mod.residual(eq, n, ins_h, X)
+            assert res.max() <= res_tol, (eq, n, v.index, b, res.max() / (n * EPS))
+            if eq == "cholesky":
+                assert np.all(np.tril(X, -1) == 0.0)
+            if eq == "lyapunov":
+                assert np.array_equal(X, np.transpose(X, (0, 2, 1)))
+
+
+def test_known_answers():
+    for n in (4, 8, 16, 64):
+        I = torch.eye(n, dtype=torch.float64, device="cuda").expand(3, n, n).contiguous()
+        for v in builtin_variants("cholesky"):
+            for b in default_blocks(n):
+                X, _ = executor.solve("cholesky", [I], variant=v.index, b=b)
+                assert torch.equal(X, I)
+    n = 8
+    L = (2.0 * torch.eye(n, dtype=torch.float64, device="cuda")).expand(2, n, n).contiguous()
+    U = (3.0 * torch.eye(n, dtype=torch.float64, device="cuda")).expand(2, n, n).contiguous()
+    C = torch.full((2, n, n), 10.0, dtype=torch.float64, device="cuda")
+    for v in builtin_variants("sylvester"):
+        X, _ = executor.solve("sylvester", [L, U, C], variant=v.index, b=4)
+        assert torch.equal(X, torch.full_like(C, 2.0))
+
+
+def test_non_spd_and_nan_are_reported():
+    n = 16
+    A = executor.generate("cholesky", n, seed=1, batch=4)[0]
+    A[2, 6, 6] = -1000.0
+    with pytest.raises(errors.VerificationError):
+        executor.solve("cholesky", [A], variant=2, b=4)
+    X, info = executor.solve("cholesky", [A], variant=2, b=4, check=False)
+    info = info.cpu().numpy()
+    assert info[2] == 7 and info[0] == 0 and info[1] == 0 and info[3] == 0
+    L, U, C = executor.generate("sylvester", n, seed=1, batch=3)
+    C[1, 0, 0] = float("nan")
+    _, info = executor.solve("sylvester", [L, U, C], variant=13, b=4, check=False)
+    assert info.cpu().tolist() == [0, -1, 0]
+    try:
+        import lagen.errors
+        with pytest.raises(lagen.errors.VerificationError):
+            executor.solve("sylvester", [L, U, C], variant=13, b=4)
+    except ImportError:
+        pass
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+def test_generator_matches_cpu_twin(eq, oracle_mod):
+    for n in (4, 36, 128):
+        dev = [t.cpu().numpy() for t in executor.generate(eq, n, seed=11, batch=5, first=1000)]
+        cpu = oracle_mod.generate(eq, n, seed=11, first=1000, batch=5)
+        for a, b in zip(dev, cpu):
+            assert np.array_equal(a == 0.0, b == 0.0)
+            np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-13)
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+def test_shard_invariance_on_device(eq):
+    n = 24
+    whole = executor.generate(eq, n, seed=7, batch=40)
+    lo = executor.generate(eq, n, seed=7, batch=17)
+    hi = executor.generate(eq, n, seed=7, batch=23, first=17)
+    for w, a, b in zip(whole, lo, hi):
+        assert torch.equal(w, torch.cat([a, b]))
+    Xw, _ = executor.solve(eq, whole)
+    Xa, _ = executor.solve(eq, lo)
+    Xb, _ = executor.solve(eq, hi)
+    assert torch.equal(Xw, torch.cat([Xa, Xb]))
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+def test_host_pipeline_equals_device_path(eq):
+    n = 32
+    ins = executor.generate(eq, n, seed=3, batch=70000 if eq == "cholesky" else 9000)
+    Xd, _ = executor.solve(eq, ins)
+    host = [t.cpu().pin_memory() for t in ins]
+    Xh, info = executor.solve_host(eq, host)
+    assert torch.equal(Xh, Xd.cpu())
+    assert int(info.abs().sum()) == 0
+
+
+def _device_residual(eq, ins, X):
+    if eq == "cholesky":
+        (A,) = ins
+        R = torch.bmm(X.transpose(1, 2), X) - A
+        rhs = A
+    elif eq == "lyapunov":
+        L, S = ins
+        R = torch.bmm(L, X) + torch.bmm(X, L.transpose(1, 2)) - S
+        rhs = S
+    else:
+        L, U, C = ins
+        R = torch.bmm(L, X) + torch.bmm(X, U) - C
+        rhs = C
+    num = torch.linalg.matrix_norm(R)
+    den = torch.clamp(torch.linalg.matrix_norm(rhs), min=1.0)
+    return (num / den).cpu().numpy()
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+@pytest.mark.parametrize("n", [16, 64, 128])
+def test_full_batch_properties(eq, n, oracle_mod):
+    """BASELINE batch floor(2^28 / 8n^2) (config 2-4 size): residual of every
+    problem, plus a sampled oracle comparison."""
+    batch = (1 << 28) // (8 * n * n)
+    ins = executor.generate(eq, n, seed=n, batch=batch)
+    X, info = executor.solve(eq, ins)
+    assert int((info != 0).sum()) == 0
+    res = _device_residual(eq, ins, X)
+    assert res.max() <= 10 * n * EPS, res.max() / (n * EPS)
+    idx = torch.randperm(batch, generator=torch.Generator().manual_seed(n))[:64].cuda()
+    sub = [t[idx].cpu().numpy() for t in ins]
+    vs = builtin_variants(eq)
+    ref, _ = oracle_mod.execute(eq, vs[0].statements, n, default_blocks(n)[0], sub)
+    assert rel_diff(X[idx].cpu().numpy(), ref).max() <= REL_TOL
+
+
+def test_reference_algorithm_objects_drop_in():
+    """The reference's own Algorithm objects run unchanged through the backend."""
+    lagen = pytest.importorskip("lagen")
+    from lagen.lang import parse_equation
+    from lagen.verify import interpret_algorithm as ref_interpret, random_instance
+    from lagen.worksheet import enumerate_algorithms
+
+    cases = {
+        "cholesky": "Equation: X^T * X = A\nA: Matrix(n,n), spd, input\nX: Matrix(n,n), upper_triangular, output\n",
+        "lyapunov": "Equation: L * X + X * L^T = S\nL: Matrix(n,n), lower_triangular, input\n"
+                    "S: Matrix(n,n), symmetric, input\nX: Matrix(n,n), symmetric, output\n",
+        "sylvester": "Equation: L * X + X * U = C\nL: Matrix(n,n), lower_triangular, input\n"
+                     "U: Matrix(n,n), upper_triangular, input\nC: Matrix(n,n), general, input\n"
+                     "X: Matrix(n,n), general, output\n",
+    }
+    for name, text in cases.items():
+        eq = parse_equation(text, name=name)
+        inst = random_instance(eq, 16, seed=42)
+        for alg in enumerate_algorithms(eq):
+            for b in (4, 8):
+                want, wflops = ref_interpret(alg, inst, b)
+                got, gflops = executor.interpret_algorithm(alg, inst, b)
+                assert gflops == wflops
+                x = want["X"]
+                assert np.linalg.norm(got["X"] - x) <= REL_TOL * max(1.0, np.linalg.norm(x))
