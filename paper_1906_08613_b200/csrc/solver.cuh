@@ -62,7 +62,7 @@ struct Policy {
   static constexpr int P1 = (P0 / WARP_P) * WARP_P > 0 ? (P0 / WARP_P) * WARP_P : WARP_P;
   static constexpr int P = G > 32 ? cmin(P1, 15) : P1;  // named barriers 1..15
   static constexpr int THREADS = G * P;
-  static constexpr size_t SMEM = (size_t)P * PS * 8 + 16 * sizeof(int);
+  static constexpr size_t SMEM = (size_t)P * PS * 8 + (((size_t)P * sizeof(int) + 15) & ~(size_t)15);  // + per-problem flags
 };
 
 // ----------------------------------------------------------------------------
