@@ -1,0 +1,530 @@
+#!/usr/bin/env python
+"""bench.py — batched fp64 GFLOP/s vs n and % of roofline on B200
+(BASELINE.json metric; SURVEY §8d definitions).
+
+A "step" is one pass of the hot path over one batch of synthetic input per
+size: by default configs[1] of BASELINE.json, the upper-Cholesky sweep over
+n in {4, 8, ..., 128} with batch floor(2^28 / 8n^2) (256 MiB of A per n),
+seed n.  The Lyapunov (configs[2]) and Sylvester (configs[3]) sweeps are
+measured the same way and reported under "extra".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W]
+                    [--workload chol-sweep|lyap-sweep|sylv-sweep|c1|c5-chol|c5-lyap|c5-sylv]
+                    [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU, NCCL only for the barrier and the
+max-over-ranks time): every rank solves its own index range of problems
+(weak scaling for the sweeps, strong scaling for c5), no data-path
+collective.
+
+Timing: W untimed warm-up steps, then K steps; the sweep is captured once
+in a CUDA graph (one kernel per size) and replayed; CUDA events on the
+launching stream, synchronize + barrier on both sides, max over ranks.
+Inputs per size are >= 256 MiB per operand (larger than the 126 MB L2)
+except c1, which flushes L2 between steps.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+SIZES = list(range(4, 129, 4))
+EQS = {"chol": "cholesky", "lyap": "lyapunov", "sylv": "sylvester"}
+NOMINAL_HBM_GBS = 8000.0        # BASELINE.md roofline (nominal)
+NOMINAL_FP64_TFLOPS = 37.2      # 148 SM x 64 FMA/clk x 2 x 1.965 GHz
+METRIC = "batched fp64 GFLOP/s vs n (n^3/3 chol; 2n^3 lyap/sylv); % of roofline"
+
+
+def measured_peaks():
+    peaks = {"hbm_gbs": None, "fp64_tflops": None, "source": {}}
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        peaks["hbm_gbs"] = d.get("hbm_gbs")
+        peaks["source"]["hbm_gbs"] = "MEASURED_PEAKS.json (measured copy)"
+    if peaks["hbm_gbs"] is None:
+        peaks["hbm_gbs"] = 6650.0
+        peaks["source"]["hbm_gbs"] = "fallback (B200_PROFILING.md)"
+    f = REPO / "profiles" / "fp64_peaks.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        peaks["fp64_tflops"] = max(d.get("dfma_tflops", 0), d.get("dmma_tflops", 0))
+        peaks["source"]["fp64_tflops"] = "profiles/fp64_peaks.json (tools/fp64_peaks.cu, measured)"
+    else:
+        peaks["fp64_tflops"] = NOMINAL_FP64_TFLOPS
+        peaks["source"]["fp64_tflops"] = "nominal"
+    return peaks
+
+
+def batch_for(n):
+    return (1 << 28) // (8 * n * n)
+
+
+def workload(name, world):
+    """(eq, [(n, batch_per_rank, seed)], scaling, description)."""
+    if name.endswith("-sweep"):
+        eq = EQS[name.split("-")[0]]
+        return eq, [(n, batch_for(n), n) for n in SIZES], "weak", \
+            f"{eq} sweep n=4..128 step 4, batch floor(2^28/8n^2) per GPU, seed n"
+    if name == "c1":
+        return "cholesky", [(16, 4096, 0)], "weak", "cholesky n=16 batch 4096 seed 0 (L2 flushed between steps)"
+    if name.startswith("c5-"):
+        eq = EQS[name.split("-")[1]]
+        total = 1 << 20
+        per = -(-total // world)
+        return eq, [(64, per, 7)], "strong", f"{eq} n=64, 2^20 problems sharded over GPUs, seed 7"
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                mask = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, v in self.REASONS.items():
+                    if mask & v and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self.nvml:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.nvml:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+# distributed plumbing
+# ----------------------------------------------------------------------------
+def dist_setup(gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        torch.distributed.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, world):
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def run_sweep(eq, cases, rank, steps, warmup, peaks, flush_l2=False, per_n_reps=None, clocks=None):
+    """Returns dict with per-step times, per-n kernel times and bookkeeping."""
+    from paper_1906_08613_b200 import executor
+    from paper_1906_08613_b200.variants import bytes_compulsory, flops_alg, flops_nominal
+
+    stream = torch.cuda.Stream()
+    plans = []
+    with torch.cuda.stream(stream):
+        for n, batch, seed in cases:
+            ins = executor.generate(eq, n, seed, batch, first=rank * batch, stream=stream)
+            plans.append(executor.Plan(eq, ins))
+    stream.synchronize()
+    # first launches (sets kernel attributes outside capture) + check
+    for p in plans:
+        p.launch(stream)
+    stream.synchronize()
+    for p in plans:
+        bad = int((p.info != 0).sum())
+        if bad:
+            raise RuntimeError(f"{eq} n={p.n}: {bad} problems reported info != 0")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if flush_l2 else None
+
+    graph = None
+    if not flush_l2:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            for p in plans:
+                p.launch(stream)
+        stream.synchronize()
+
+    def one_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            for p in plans:
+                p.launch(stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            if flush is not None:
+                flush.fill_(1)
+            one_step()
+    stream.synchronize()
+    times = []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    with (clocks or _Null()):
+        with torch.cuda.stream(stream):
+            for i in range(steps):
+                if flush is not None:
+                    flush.fill_(1)
+                ev[i][0].record(stream)
+                one_step()
+                ev[i][1].record(stream)
+        stream.synchronize()
+    times = [a.elapsed_time(b) for a, b in ev]
+
+    # per-size kernel times (events around each launch; median of reps)
+    reps = per_n_reps or max(3, min(steps, 10))
+    per_n = []
+    with torch.cuda.stream(stream):
+        for p in plans:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(reps)]
+            for a, b in evs:
+                if flush is not None:
+                    flush.fill_(1)
+                a.record(stream)
+                p.launch(stream)
+                b.record(stream)
+            stream.synchronize()
+            ms = statistics.median(x.elapsed_time(y) for x, y in evs)
+            n, batch = p.n, p.batch
+            f_nom, f_alg, byt = flops_nominal(eq, n), flops_alg(eq, n), bytes_compulsory(eq, n)
+            t = ms * 1e-3
+            t_roof_nom = batch * max(f_alg / (NOMINAL_FP64_TFLOPS * 1e12), byt / (NOMINAL_HBM_GBS * 1e9))
+            t_roof_meas = batch * max(f_alg / (peaks["fp64_tflops"] * 1e12), byt / (peaks["hbm_gbs"] * 1e9))
+            per_n.append({
+                "n": n, "batch": batch, "variant": p.variant, "b": p.b, "ms": round(ms, 5),
+                "gflops": round(batch * f_nom / t / 1e9, 1),
+                "gflops_alg": round(batch * f_alg / t / 1e9, 1),
+                "gbs": round(batch * byt / t / 1e9, 1),
+                "bound": "hbm" if byt / (peaks["hbm_gbs"] * 1e9) >= f_alg / (peaks["fp64_tflops"] * 1e12) else "fp64",
+                "roofline_frac_nominal": round(t_roof_nom / t, 4),
+                "roofline_frac_measured": round(t_roof_meas / t, 4),
+            })
+    out = {"times_ms": times, "per_n": per_n, "plans": plans, "stream": stream,
+           "flops_nominal": sum(p.batch * flops_nominal(eq, p.n) for p in plans),
+           "flops_alg": sum(p.batch * flops_alg(eq, p.n) for p in plans),
+           "bytes": sum(p.batch * bytes_compulsory(eq, p.n) for p in plans),
+           "launches_per_step": len(plans)}
+    return out
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def run_e2e(eq, plans, steps, world):
+    """Same workload through the public host-buffer API: H2D of the inputs
+    from pinned memory, solve, D2H of X and info, every step."""
+    from paper_1906_08613_b200 import executor
+    hosts = []
+    for p in plans:
+        ins = [t.cpu().pin_memory() for t in p.inputs]
+        out = torch.empty_like(ins[0]).pin_memory()
+        info = torch.empty(p.batch, dtype=torch.int32).pin_memory()
+        hosts.append((p, ins, out, info))
+    h2d = sum(sum(t.numel() * 8 for t in ins) for _, ins, _, _ in hosts)
+    d2h = sum(out.numel() * 8 + info.numel() * 4 for _, _, out, info in hosts)
+    # warm-up one pass
+    for p, ins, out, info in hosts:
+        executor.solve_host(eq, ins, variant=p.variant, b=p.b, out=out, info=info)
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        for p, ins, out, info in hosts:
+            executor.solve_host(eq, ins, variant=p.variant, b=p.b, out=out, info=info)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    barrier(world)
+    dt = max_over_ranks(dt, world)
+    # correctness of what came back
+    for p, ins, out, info in hosts[-1:]:
+        assert torch.equal(out, p.out.cpu()), "host pipeline result differs from device path"
+    return dt / steps, h2d, d2h
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline (reference's emitted C through oracle/_ref, else the port)
+# ----------------------------------------------------------------------------
+def cpu_baseline(eq, cases, budget_s=12.0, inputs_from=None, seed_first=0):
+    """Time the reference CPU path on a bounded sample of each size; value is
+    the throughput it would sustain on the full workload (problems are
+    independent, so time scales linearly with the batch)."""
+    from oracle import build_ref, oracle
+    from paper_1906_08613_b200.variants import builtin_variants, default_blocks, flops_nominal
+
+    cores = len(os.sched_getaffinity(0))
+    use_ref = build_ref.available()
+    ref = build_ref.RefLib() if use_ref else None
+    per_size_budget = budget_s / len(cases)
+    tot_flops, tot_time, detail = 0.0, 0.0, []
+    for ci, (n, batch, seed) in enumerate(cases):
+        # sample size: aim at ~per_size_budget/2 for the timed run
+        est_ns = {"cholesky": 0.35, "lyapunov": 0.8, "sylvester": 1.1}[eq] * n ** 3 / cores
+        s = int(max(cores, min(batch, per_size_budget * 0.5 / (est_ns * 1e-9))))
+        if inputs_from is not None:
+            ins = [t[:s].cpu().numpy() for t in inputs_from[ci]]
+        else:
+            ins = oracle.generate(eq, n, seed, seed_first, s)
+        if ref is not None:
+            cands = ref.kernels(eq, n)
+            best = None
+            probe = [a[: max(cores, s // 8)] for a in ins]
+            for idx, k in cands:
+                ref.run(idx, probe)
+                t0 = time.perf_counter()
+                ref.run(idx, probe)
+                dt = time.perf_counter() - t0
+                if best is None or dt < best[0]:
+                    best = (dt, idx, k)
+            _, idx, k = best
+            ref.run(idx, [a[:cores] for a in ins])
+            t0 = time.perf_counter()
+            ref.run(idx, ins)
+            dt = time.perf_counter() - t0
+            which = k["name"]
+        else:
+            v = builtin_variants(eq)[0]
+            b = default_blocks(n)[0]
+            t0 = time.perf_counter()
+            oracle.execute(eq, v.statements, n, b, ins, nthreads=cores)
+            dt = time.perf_counter() - t0
+            which = f"oracle port v0 b{b}"
+        t_full = dt * batch / s
+        tot_flops += batch * flops_nominal(eq, n)
+        tot_time += t_full
+        detail.append({"n": n, "sample": s, "kernel": which, "gflops": round(s * flops_nominal(eq, n) / dt / 1e9, 2)})
+    return {
+        "value": round(tot_flops / tot_time / 1e9, 2), "unit": "GFLOP/s", "cores": cores,
+        "kind": "reference" if use_ref else "port",
+        "sample": (f"per size: the first s problems of the same workload (s sized for ~{per_size_budget:.2f} s), "
+                   "throughput extrapolated to the full batch; kernel = fastest verified emitted variant "
+                   "(lagen emit_function, nu=4) compiled gcc -O3 -march=native -std=c99, OpenMP over problems")
+        if use_ref else "oracle C port, OpenMP over problems",
+        "cpu_model": _cpu_model(), "per_n": detail,
+    }
+
+
+def _cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+# ----------------------------------------------------------------------------
+def summarize(eq, res, steps, peaks, world):
+    ms = statistics.mean(res["times_ms"])
+    ms = max_over_ranks(ms, world)
+    flops = sum_over_ranks(res["flops_nominal"], world)
+    value = flops / (ms * 1e-3) / 1e9
+    # roofline of the sweep's kernels: algorithmic bytes (or flops) per launch
+    # over the measured launch time, aggregated over the step's launches
+    t_kernels = sum(r["ms"] for r in res["per_n"]) * 1e-3
+    achieved_gbs = res["bytes"] / t_kernels / 1e9
+    achieved_tf = res["flops_alg"] / t_kernels / 1e12
+    hbm_time = res["bytes"] / (peaks["hbm_gbs"] * 1e9)
+    fp_time = res["flops_alg"] / (peaks["fp64_tflops"] * 1e12)
+    if hbm_time >= fp_time:
+        roof = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved_gbs / peaks["hbm_gbs"], 4)}
+    else:
+        roof = {"bound": "fp64", "achieved": round(achieved_tf, 3), "peak": peaks["fp64_tflops"],
+                "unit": "TFLOP/s", "frac": round(achieved_tf / peaks["fp64_tflops"], 4)}
+    t_roof_nom = sum(r["batch"] * 0 + r["ms"] * r["roofline_frac_nominal"] for r in res["per_n"]) * 1e-3
+    roof["frac_of_nominal_roofline"] = round(t_roof_nom / t_kernels, 4)
+    roof["traffic"] = None
+    return value, ms, roof
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="chol-sweep")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sizes", default=None, help="comma-separated subset of n (debug)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the lyap/sylv sweeps")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--json-out", default=None)
+    args = ap.parse_args()
+    if args.sizes:
+        global SIZES
+        SIZES = [int(x) for x in args.sizes.split(",")]
+    warmup = max(3, args.warmup)
+
+    if args.impl == "reference":
+        return reference_arm(args, warmup)
+
+    world, rank, local = dist_setup(args.gpus)
+    peaks = measured_peaks()
+    eq, cases, scaling, desc = workload(args.workload, world)
+    clocks = ClockSampler(local)
+    barrier(world)
+    res = run_sweep(eq, cases, rank, args.steps, warmup, peaks, flush_l2=(args.workload == "c1"),
+                    clocks=clocks)
+    value, ms, roof = summarize(eq, res, args.steps, peaks, world)
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: seeded counter-based generator, BASELINE.json distributions (no dataset)",
+        "config": {"workload": args.workload, "description": desc, "sizes": [c[0] for c in cases],
+                   "batch_per_gpu": {str(c[0]): c[1] for c in cases},
+                   "l2": "flush 256 MiB between steps" if args.workload == "c1" else
+                   "inputs > L2 (>= 256 MiB per operand per size)",
+                   "variant_selection": "dispatch_table.json (GPU autotune of every variant x b) "
+                                        "else static fallback",
+                   "timing": "sweep captured in one CUDA graph; CUDA events on the launching stream"},
+        "roofline": roof,
+        "gpu_launches": res["launches_per_step"] * args.steps,
+        "clocks": clocks.summary(),
+        "peaks": peaks,
+        "per_n": res["per_n"],
+    }
+    if not args.no_e2e:
+        e2e_steps = max(1, min(2, args.steps))
+        dt, h2d, d2h = run_e2e(eq, res["plans"], e2e_steps, world)
+        line["e2e"] = {"value": round(sum_over_ranks(res["flops_nominal"], world) / dt / 1e9, 2),
+                       "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                       "steps": e2e_steps,
+                       "path": "executor.solve_host -> lagen_b200_execute_host (pinned host buffers, "
+                               "chunked H2D/solve/D2H over two streams)"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(eq, cases, budget_s=args.cpu_budget,
+                                            inputs_from=[p.inputs for p in res["plans"]])
+    # free before the secondary sweeps
+    del res
+    torch.cuda.empty_cache()
+    if args.workload == "chol-sweep" and not args.no_extra:
+        extra = {}
+        for wl in ("lyap-sweep", "sylv-sweep"):
+            eq2, cases2, _, desc2 = workload(wl, world)
+            r2 = run_sweep(eq2, cases2, rank, args.steps, warmup, peaks)
+            v2, ms2, roof2 = summarize(eq2, r2, args.steps, peaks, world)
+            extra[eq2] = {"value": round(v2, 2), "unit": "GFLOP/s", "ms_per_step": round(ms2, 4),
+                          "roofline": roof2, "per_n": r2["per_n"], "description": desc2}
+            if rank == 0 and world == 1 and not args.no_cpu:
+                extra[eq2]["cpu_baseline"] = cpu_baseline(eq2, cases2, budget_s=args.cpu_budget,
+                                                          inputs_from=[p.inputs for p in r2["plans"]])
+            del r2
+            torch.cuda.empty_cache()
+        line["extra"] = extra
+    if rank == 0:
+        text = json.dumps(line)
+        print(text, flush=True)
+        if args.json_out:
+            Path(args.json_out).write_text(json.dumps(line, indent=1) + "\n")
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def reference_arm(args, warmup):
+    """The reference's own CPU implementation of the path (oracle/_ref: the
+    emitted kernels compiled here with the reference's flags) on the host
+    cores, same workload/metric; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    eq, cases, scaling, desc = workload(args.workload, 1)
+    # each step: a bounded sample of every size, throughput extrapolated
+    budget = max(1.0, 60.0 / (args.steps + warmup))
+    for _ in range(warmup):
+        cpu_baseline(eq, cases, budget_s=budget / 4)
+    vals = []
+    t0 = time.perf_counter()
+    base = None
+    for _ in range(args.steps):
+        base = cpu_baseline(eq, cases, budget_s=budget)
+        vals.append(base["value"])
+    dt = time.perf_counter() - t0
+    value = statistics.median(vals)
+    base["value"] = value
+    line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": warmup, "ms_per_step": round(dt / args.steps * 1e3, 2), "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded counter-based generator (CPU twin), BASELINE.json distributions",
+            "config": {"workload": args.workload, "description": desc, "sizes": [c[0] for c in cases]},
+            "impl": "reference", "cpu_baseline": base,
+            "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main() or 0)

@@ -129,6 +129,42 @@ def solve(eq, inputs, variant=None, b=None, out=None, info=None, stream=None, ch
     return out, info
 
 
+class Plan:
+    """A prepared batched solve: arguments marshalled once, launched many
+    times (no per-call validation or allocation) — suitable for CUDA-graph
+    capture of a whole sweep."""
+
+    def __init__(self, eq, inputs, variant=None, b=None, out=None, info=None):
+        self.eq = _eq_name(eq)
+        self.batch, self.n = _check_inputs(self.eq, inputs)
+        stmts, idx = resolve_variant(self.eq, variant)
+        if stmts is None:
+            pick = dispatch.select(self.eq, self.n)
+            idx = pick["variant"]
+            stmts = builtin_variants(self.eq)[idx].statements
+            b = b or pick["b"]
+        if b is None:
+            b = dispatch.select(self.eq, self.n)["b"]
+        validate(self.eq, stmts)
+        self.variant, self.b, self.stmts = idx, b, stmts
+        dev = inputs[0].device
+        self.inputs = list(inputs)
+        self.out = out if out is not None else torch.empty((self.batch, self.n, self.n),
+                                                           dtype=torch.float64, device=dev)
+        self.info = info if info is not None else torch.empty(self.batch, dtype=torch.int32, device=dev)
+        self._arr = _lib.stmt_array(stmts)
+        self._ptrs = (ctypes.c_void_p * 3)(*([t.data_ptr() for t in inputs] + [0] * (3 - len(inputs))))
+        self._args = (EQ_CODES[self.eq], ctypes.addressof(self._arr), len(stmts), self.n, b, self.batch,
+                      ctypes.addressof(self._ptrs), ctypes.c_void_p(self.out.data_ptr()),
+                      ctypes.c_void_p(self.info.data_ptr()))
+        self.device = dev
+
+    def launch(self, stream=None):
+        rc = _lib.lib.lagen_b200_execute(*self._args, _stream_ptr(stream))
+        _lib.check(rc, f"{self.eq} n={self.n} b={self.b}")
+        return self.out
+
+
 def execute_batched(alg, n, b, inputs, stream=None, check=True):
     """SURVEY §8b Python side: semantics of interpret_algorithm over a batch.
 
@@ -141,8 +177,8 @@ def execute_batched(alg, n, b, inputs, stream=None, check=True):
     else:
         eq_name = _eq_name(alg.equation)
     tensors = [inputs[nm] for nm in EQ_INPUTS[eq_name]]
-    X, _ = solve(eq_name, tensors, variant=alg, b=b, stream=stream, check=check)
     _check_inputs(eq_name, tensors, n)
+    X, _ = solve(eq_name, tensors, variant=alg, b=b, stream=stream, check=check)
     return {"X": X}
 
 
