@@ -109,6 +109,18 @@ int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b
                        long long batch, const double* const* inputs, double* X,
                        int* info, void* stream);
 
+/* Engine selection: LAGEN_ENGINE_AUTO picks the compiled-in
+ * "warp engine" instance when the statement list equals a built-in variant
+ * that has one for (n, b), else the generic statement-list kernel. */
+#define LAGEN_ENGINE_AUTO 0
+#define LAGEN_ENGINE_GENERIC 1
+#define LAGEN_ENGINE_WARP 2
+int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
+                              long long batch, const double* const* inputs, double* X,
+                              int* info, void* stream, int engine);
+/* 1 if the warp engine has an instance for (eq, n, b, built-in variant) */
+int lagen_b200_warp_supported(int eq, int n, int b, int variant);
+
 /* Same, but every buffer is in HOST memory (pinned for full overlap).  The
  * batch is streamed through the device in chunks, H2D copy / solve / D2H copy
  * pipelined over two streams; synchronous on return. */

@@ -11,6 +11,7 @@
 #include "inst_index.h"
 #include "lagen_b200.h"
 #include "registry.cuh"
+#include "registry_warp.cuh"
 #include "variants_table.h"
 
 using namespace lagen;
@@ -26,6 +27,39 @@ int fail(int code, const std::string& msg) {
 
 int cuda_fail(cudaError_t e, const char* where) {
   return fail(LAGEN_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+const WarpEntry* find_warp(int eq, int n, int b, int variant) {
+  if (eq < 0 || eq > 2 || variant < 0) return nullptr;
+  for (int p = 0; p < kWarpParts; ++p) {
+    const WarpTable& t = kWarpTables[eq][p];
+    for (int i = 0; i < *t.n; ++i)
+      if (t.e[i].n == n && t.e[i].b == b && t.e[i].variant == variant) return &t.e[i];
+  }
+  return nullptr;
+}
+
+const lagen_stmt* builtin(int eq, int variant, int* count);
+
+// index of the built-in variant whose statement list equals stmts, or -1
+int match_builtin(int eq, const lagen_stmt* stmts, int nstmts) {
+  for (int v = 0;; ++v) {
+    int count = 0;
+    const lagen_stmt* s = builtin(eq, v, &count);
+    if (!s) return -1;
+    if (count != nstmts) continue;
+    bool same = true;
+    for (int k = 0; k < count && same; ++k) {
+      const lagen_stmt& a = s[k];
+      const lagen_stmt& b = stmts[k];
+      same = a.kind == b.kind && a.sign == b.sign && a.out.op == b.out.op && a.out.r == b.out.r &&
+             a.out.c == b.out.c;
+      for (int j = 0; j < 2 && same; ++j)
+        same = a.in[j].op == b.in[j].op && (a.in[j].op < 0 || (a.in[j].r == b.in[j].r && a.in[j].c == b.in[j].c &&
+                                                              a.in[j].trans == b.in[j].trans));
+    }
+    if (same) return v;
+  }
 }
 
 const KernelEntry* find_entry(int eq, int n, int b) {
@@ -158,8 +192,16 @@ int lagen_b200_geometry(int eq, int n, int b, int* g, int* p, int* threads, int*
   return LAGEN_OK;
 }
 
+int lagen_b200_warp_supported(int eq, int n, int b, int variant) { return find_warp(eq, n, b, variant) ? 1 : 0; }
+
 int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                        const double* const* inputs, double* X, int* info, void* stream) {
+  return lagen_b200_execute_engine(eq, stmts, nstmts, n, b, batch, inputs, X, info, stream, LAGEN_ENGINE_AUTO);
+}
+
+int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
+                              const double* const* inputs, double* X, int* info, void* stream, int engine) {
+  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_WARP) return fail(LAGEN_EINVAL, "unknown engine");
   int rc = check_common(eq, n, b, batch);
   if (rc) return rc;
   rc = validate(eq, stmts, nstmts);
@@ -176,8 +218,15 @@ int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b
   a.X = X;
   a.info = info;
   a.batch = batch;
-  const KernelEntry* e = find_entry(eq, n, b);
-  cudaError_t err = e->launch(a, static_cast<cudaStream_t>(stream));
+  const WarpEntry* w = nullptr;
+  if (engine != LAGEN_ENGINE_GENERIC) {
+    const int v = match_builtin(eq, stmts, nstmts);
+    w = find_warp(eq, n, b, v);
+    if (!w && engine == LAGEN_ENGINE_WARP)
+      return fail(LAGEN_EUNSUPPORTED, "no warp-engine instance for this (variant, n, b)");
+  }
+  cudaError_t err = w ? w->launch(a, static_cast<cudaStream_t>(stream))
+                      : find_entry(eq, n, b)->launch(a, static_cast<cudaStream_t>(stream));
   if (err != cudaSuccess) return cuda_fail(err, "solve launch");
   return LAGEN_OK;
 }

@@ -33,6 +33,7 @@ def reload():
 def select(eq_name, n):
     entry = _table().get(eq_name, {}).get(str(n))
     if entry is not None:
-        return {"variant": int(entry["variant"]), "b": int(entry["b"]), "source": "autotune"}
+        return {"variant": int(entry["variant"]), "b": int(entry["b"]), "source": "autotune",
+                "engine": entry.get("engine", "auto")}
     blocks = default_blocks(n) or [4]
     return {"variant": _FALLBACK_VARIANT[eq_name], "b": max(blocks), "source": "fallback"}

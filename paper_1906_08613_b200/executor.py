@@ -88,7 +88,7 @@ def _check_inputs(eq_name, inputs, n=None):
     return shape[0], shape[1]
 
 
-def solve(eq, inputs, variant=None, b=None, out=None, info=None, stream=None, check=True):
+def solve(eq, inputs, variant=None, b=None, out=None, info=None, stream=None, check=True, engine="auto"):
     """Solve a batch: inputs in _signature order (chol: A; lyap: L, S;
     sylv: L, U, C), each [batch, n, n] float64 CUDA contiguous.
 
@@ -114,9 +114,10 @@ def solve(eq, inputs, variant=None, b=None, out=None, info=None, stream=None, ch
     arr = _lib.stmt_array(stmts)
     ptrs = (ctypes.c_void_p * 3)(*([t.data_ptr() for t in inputs] + [0] * (3 - len(inputs))))
     with torch.cuda.device(dev):
-        rc = _lib.lib.lagen_b200_execute(EQ_CODES[eq_name], ctypes.addressof(arr), len(stmts), n, b,
-                                         batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
-                                         ctypes.c_void_p(info.data_ptr()), _stream_ptr(stream))
+        rc = _lib.lib.lagen_b200_execute_engine(EQ_CODES[eq_name], ctypes.addressof(arr), len(stmts), n, b,
+                                                batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
+                                                ctypes.c_void_p(info.data_ptr()), _stream_ptr(stream),
+                                                _lib.ENGINES[engine])
     _lib.check(rc, f"{eq_name} n={n} b={b}")
     if check and batch:
         bad = torch.nonzero(info).flatten()
@@ -134,7 +135,7 @@ class Plan:
     times (no per-call validation or allocation) — suitable for CUDA-graph
     capture of a whole sweep."""
 
-    def __init__(self, eq, inputs, variant=None, b=None, out=None, info=None):
+    def __init__(self, eq, inputs, variant=None, b=None, out=None, info=None, engine=None):
         self.eq = _eq_name(eq)
         self.batch, self.n = _check_inputs(self.eq, inputs)
         stmts, idx = resolve_variant(self.eq, variant)
@@ -143,10 +144,12 @@ class Plan:
             idx = pick["variant"]
             stmts = builtin_variants(self.eq)[idx].statements
             b = b or pick["b"]
+            engine = engine or pick.get("engine")
         if b is None:
             b = dispatch.select(self.eq, self.n)["b"]
         validate(self.eq, stmts)
         self.variant, self.b, self.stmts = idx, b, stmts
+        self.engine = engine or "auto"
         dev = inputs[0].device
         self.inputs = list(inputs)
         self.out = out if out is not None else torch.empty((self.batch, self.n, self.n),
@@ -160,7 +163,7 @@ class Plan:
         self.device = dev
 
     def launch(self, stream=None):
-        rc = _lib.lib.lagen_b200_execute(*self._args, _stream_ptr(stream))
+        rc = _lib.lib.lagen_b200_execute_engine(*self._args, _stream_ptr(stream), _lib.ENGINES[self.engine])
         _lib.check(rc, f"{self.eq} n={self.n} b={self.b}")
         return self.out
 

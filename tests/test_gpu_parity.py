@@ -22,8 +22,8 @@ import torch
 pytestmark = pytest.mark.gpu
 
 from paper_1906_08613_b200 import errors, executor  # noqa: E402
-from paper_1906_08613_b200.variants import (EQ_INPUTS, EQUATIONS, builtin_variants,  # noqa: E402
-                                             default_blocks)
+from paper_1906_08613_b200.variants import (EQ_CODES, EQ_INPUTS, EQUATIONS,  # noqa: E402
+                                             builtin_variants, default_blocks)
 
 EPS = np.finfo(np.float64).eps
 REL_TOL = 1e-10
@@ -55,9 +55,13 @@ def test_golden_reference_vectors(eq):
     groups = {}
     for e in META[eq]["entries"]:
         groups.setdefault((e["n"], e["variant"], e["b"]), []).append(e)
+    from paper_1906_08613_b200 import _lib
     for (n, v, b), es in groups.items():
+      for engine in ("generic", "warp"):
+        if engine == "warp" and not _lib.lib.lagen_b200_warp_supported(EQ_CODES[eq], n, b, v):
+            continue
         ins = [np.stack([d[f"in_{e['case']}_{n}_{nm}"] for e in es]) for nm in EQ_INPUTS[eq]]
-        X, info = executor.solve(eq, to_dev(ins), variant=v, b=b)
+        X, info = executor.solve(eq, to_dev(ins), variant=v, b=b, engine=engine)
         X = X.cpu().numpy()
         want = np.stack([d[e["key"]] for e in es])
         assert (info.cpu().numpy() == 0).all()
@@ -84,15 +88,19 @@ def test_every_variant_vs_oracle(eq, n, oracle_mod):
     ref_X, ref_info = oracle_mod.execute(eq, vs[0].statements, n, default_blocks(n)[0], ins_h)
     assert (ref_info == 0).all()
     res_tol = 10 * n * EPS
-    for v in vs:
-        for b in default_blocks(n):
-            X, info = executor.solve(eq, ins_d, variant=v.index, b=b)
+    from paper_1906_08613_b200 import _lib
+    runs = [(v, b, "generic") for v in vs for b in default_blocks(n)]
+    runs += [(v, b, "warp") for v in vs for b in default_blocks(n)
+             if _lib.lib.lagen_b200_warp_supported(EQ_CODES[eq], n, b, v.index)]
+    for v, b, engine in runs:
+        if True:
+            X, info = executor.solve(eq, ins_d, variant=v.index, b=b, engine=engine)
             X = X.cpu().numpy()
-            assert (info.cpu().numpy() == 0).all()
+            assert (info.cpu().numpy() == 0).all(), (eq, n, v.index, b, engine)
             err = rel_diff(X, ref_X).max()
-            assert err <= REL_TOL, (eq, n, v.index, b, err)
+            assert err <= REL_TOL, (eq, n, v.index, b, engine, err)
             res = oracle_mod.residual(eq, n, ins_h, X)
-            assert res.max() <= res_tol, (eq, n, v.index, b, res.max() / (n * EPS))
+            assert res.max() <= res_tol, (eq, n, v.index, b, engine, res.max() / (n * EPS))
             if eq == "cholesky":
                 assert np.all(np.tril(X, -1) == 0.0)
             if eq == "lyapunov":

@@ -26,11 +26,16 @@ from paper_1906_08613_b200 import executor  # noqa: E402
 from paper_1906_08613_b200.variants import EQUATIONS, builtin_variants, default_blocks  # noqa: E402
 
 
+def _lib_eq(eq):
+    return EQUATIONS.index(eq)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default=",".join(str(n) for n in range(4, 129, 4)))
     ap.add_argument("--eqs", default=",".join(EQUATIONS))
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--engines", default="all")
     ap.add_argument("--out", default=str(REPO / "paper_1906_08613_b200" / "dispatch_table.json"))
     ap.add_argument("--report", default=str(REPO / "gpurun_out" / "autotune_report.json"))
     args = ap.parse_args()
@@ -49,9 +54,15 @@ def main():
             stream.synchronize()
             rows = []
             ref_X = None
-            for v in builtin_variants(eq):
-                for b in default_blocks(n):
-                    plan = executor.Plan(eq, ins, variant=v.index, b=b)
+            from paper_1906_08613_b200 import _lib
+            cands = [(v, b, "generic") for v in builtin_variants(eq) for b in default_blocks(n)]
+            cands += [(v, b, "warp") for v in builtin_variants(eq) for b in default_blocks(n)
+                      if _lib.lib.lagen_b200_warp_supported(_lib_eq(eq), n, b, v.index)]
+            if args.engines != "all":
+                cands = [c for c in cands if c[2] in args.engines.split(",")]
+            for v, b, engine in cands:
+                if True:
+                    plan = executor.Plan(eq, ins, variant=v.index, b=b, engine=engine)
                     with torch.cuda.stream(stream):
                         plan.launch(stream)
                         plan.launch(stream)
@@ -72,17 +83,20 @@ def main():
                             e.record(stream)
                     stream.synchronize()
                     ms = statistics.median(a.elapsed_time(e) for a, e in evs)
-                    rows.append({"variant": v.index, "b": b, "ms": round(ms, 5), "ok": ok})
+                    rows.append({"variant": v.index, "b": b, "engine": engine, "ms": round(ms, 5), "ok": ok})
                     del plan
             good = [r for r in rows if r["ok"]]
             best = min(good, key=lambda r: (r["ms"], r["variant"], r["b"]))
-            table[eq][str(n)] = {"variant": best["variant"], "b": best["b"], "ms": best["ms"]}
+            table[eq][str(n)] = {"variant": best["variant"], "b": best["b"], "engine": best["engine"],
+                                 "ms": best["ms"]}
             report[eq][str(n)] = rows
-            print(f"{eq} n={n}: best v{best['variant']} b{best['b']} {best['ms']:.4f} ms "
+            print(f"{eq} n={n}: best v{best['variant']} b{best['b']} {best['engine']} {best['ms']:.4f} ms "
                   f"(worst {max(r['ms'] for r in rows):.4f} ms)", flush=True)
             del ins, ref_X
             torch.cuda.empty_cache()
     Path(args.out).write_text(json.dumps(table, indent=1) + "\n")
+    Path(args.report).parent.mkdir(exist_ok=True)
+    (Path(args.report).parent / "dispatch_table.json").write_text(json.dumps(table, indent=1) + "\n")
     Path(args.report).parent.mkdir(exist_ok=True)
     Path(args.report).write_text(json.dumps(report, indent=1) + "\n")
 
