@@ -109,17 +109,21 @@ int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b
                        long long batch, const double* const* inputs, double* X,
                        int* info, void* stream);
 
-/* Engine selection: LAGEN_ENGINE_AUTO picks the compiled-in
- * "warp engine" instance when the statement list equals a built-in variant
- * that has one for (n, b), else the generic statement-list kernel. */
+/* Engine selection: LAGEN_ENGINE_AUTO picks, for a statement
+ * list equal to a built-in variant, the register-resident "column engine"
+ * (Cholesky, n <= 64) or the compiled-in "warp engine" when they have an
+ * instance for (n, b); otherwise the generic statement-list kernel. */
 #define LAGEN_ENGINE_AUTO 0
 #define LAGEN_ENGINE_GENERIC 1
 #define LAGEN_ENGINE_WARP 2
+#define LAGEN_ENGINE_COLUMN 3
 int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
                               long long batch, const double* const* inputs, double* X,
                               int* info, void* stream, int engine);
 /* 1 if the warp engine has an instance for (eq, n, b, built-in variant) */
 int lagen_b200_warp_supported(int eq, int n, int b, int variant);
+/* 1 if `engine` has an instance for (eq, n, b, built-in variant) */
+int lagen_b200_engine_supported(int eq, int n, int b, int variant, int engine);
 
 /* Same, but every buffer is in HOST memory (pinned for full overlap).  The
  * batch is streamed through the device in chunks, H2D copy / solve / D2H copy

@@ -41,6 +41,7 @@ def _load():
     lib.lagen_b200_execute.argtypes = [i, vp, i, i, i, ll, vp, vp, vp, vp]
     lib.lagen_b200_execute_engine.argtypes = [i, vp, i, i, i, ll, vp, vp, vp, vp, i]
     lib.lagen_b200_warp_supported.argtypes = [i, i, i, i]
+    lib.lagen_b200_engine_supported.argtypes = [i, i, i, i, i]
     lib.lagen_b200_execute_host.argtypes = [i, vp, i, i, i, ll, vp, vp, vp]
     lib.lagen_b200_generate.argtypes = [i, i, ctypes.c_ulonglong, ll, ll, vp, vp]
     lib.lagen_b200_cholesky.argtypes = [i, i, i, ll, vp, vp, vp, vp]
@@ -57,9 +58,13 @@ EXPORTED = (
     "lagen_b200_variant_stmts", "lagen_b200_supported", "lagen_b200_geometry",
     "lagen_b200_cholesky", "lagen_b200_lyapunov", "lagen_b200_sylvester",
     "lagen_b200_execute", "lagen_b200_execute_host", "lagen_b200_generate",
-    "lagen_b200_execute_engine", "lagen_b200_warp_supported",
+    "lagen_b200_execute_engine", "lagen_b200_warp_supported", "lagen_b200_engine_supported",
 )
-ENGINES = {"auto": 0, "generic": 1, "warp": 2}
+ENGINES = {"auto": 0, "generic": 1, "warp": 2, "column": 3}
+
+
+def engine_supported(eq_code, n, b, variant, engine):
+    return bool(lib.lagen_b200_engine_supported(eq_code, n, b, variant, ENGINES[engine]))
 
 
 def check(rc, what):

@@ -3,19 +3,22 @@
 // variant's statement list compiled in (template type list generated from
 // the reference's enumerate_algorithms() output, variants_ct.cuh), GEMM
 // updates on the FP64 tensor path (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4),
-// warp-synchronous everything else (no CTA barriers).
+// warp-synchronous everything else (no CTA barriers), and the next problem
+// prefetched with cp.async while the current one is solved.
 //
 // Semantics per statement kind follow the reference block kernels
 // (kernels.py:16-130) exactly as solver.cuh documents; only the schedule and
-// summation order differ (parity <= 1e-10, BASELINE north_star).
+// summation order differ (parity <= 1e-10, BASELINE north_star).  Pivots use
+// x_ii = a_ii * rsqrt(a_ii), x_ij = a_ij * rsqrt(a_ii) and the triangular
+// solves multiply by precomputed reciprocals (<= 2 ulp from sqrt / divide).
 //
 // Tile layout (per matrix): n x n split into T x T tiles of 4x4 doubles
 // (128 B = one full bank sweep).  Element (r, c) of tile (R, C) lives at
-//   tile_index(R, C) * 16 + swz(R, C, (r&3)*4 + (c&3))
-// where swz XORs the 16-byte chunk id (0..7) with (R ^ C) & 7.  Result:
-// DMMA fragment loads (16 lanes per tile, either orientation), lane-per-row
-// and lane-per-column walks and lane-per-tile walks are all conflict-free,
-// and (c, c+1) pairs with even c stay adjacent for 16-byte accesses.
+//   tile_index(R, C) * 16 + ((chunk ^ ((R ^ C) & 7)) << 1 | (c & 1)),
+//   chunk = (r & 3) * 2 + (c & 3) / 2   (16-byte chunk inside the tile)
+// DMMA fragments (16 lanes per tile, either orientation), lane-per-row,
+// lane-per-column and lane-per-tile walks are all conflict-free, and 16-byte
+// cp.async chunks keep (c, c+1) pairs adjacent.
 // tile_index: DENSE R*T+C; UPPER (C >= R) packed rows; LOWER (C <= R).
 #pragma once
 #include <cuda_runtime.h>
@@ -31,8 +34,13 @@ namespace eng {
 enum { DENSE = 0, UPPER = 1, LOWER = 2 };
 enum { K_GEMM = 0, K_CHOL = 1, K_TRSM = 2, K_SYLV = 3, K_LYAP = 4 };
 
+__device__ __forceinline__ int swz(int r, int c, int key) {
+  return (((((r & 3) << 1) | ((c & 3) >> 1)) ^ key) << 1) | (c & 1);
+}
+
 template <int T, int LY>
 struct TM {
+  static constexpr bool GLOBAL = false;
   static constexpr int TILES = LY == DENSE ? T * T : T * (T + 1) / 2;
   static constexpr int DOUBLES = TILES * 16;
   __device__ static __forceinline__ int tidx(int R, int C) {
@@ -40,20 +48,55 @@ struct TM {
     else if constexpr (LY == UPPER) return R * T - ((R * (R - 1)) >> 1) + (C - R);
     else return ((R * (R + 1)) >> 1) + C;
   }
+  // tile-index step when R -> R + 1 at fixed C
+  __device__ static __forceinline__ int dR(int R) {
+    if constexpr (LY == DENSE) return T;
+    else if constexpr (LY == UPPER) return T - R - 1;
+    else return R + 1;
+  }
   __device__ static __forceinline__ int off(int r, int c) {
     const int R = r >> 2, C = c >> 2;
-    const int e = ((r & 3) << 2) | (c & 3);
-    const int sw = ((((e >> 1) ^ (R ^ C)) & 7) << 1) | (e & 1);
-    return (tidx(R, C) << 4) + sw;
+    return (tidx(R, C) << 4) + swz(r, c, (R ^ C) & 7);
   }
 };
 
 // Row-major global-memory operand (coefficients that do not fit on chip).
 template <int N>
 struct GM {
+  static constexpr bool GLOBAL = true;
   static constexpr int TILES = 0;
   static constexpr int DOUBLES = 0;
   __device__ static __forceinline__ int off(int r, int c) { return r * N + c; }
+};
+
+// k-walker: address of element (r, c) advanced by 4 rows (ADV_R) or 4
+// columns per step, with O(1) integer work per step.
+template <class M, bool ADV_R>
+struct KW {
+  int tp, R, C, e;
+  __device__ __forceinline__ void init(int r, int c) {
+    R = r >> 2;
+    C = c >> 2;
+    tp = M::tidx(R, C) << 4;
+    e = (((r & 3) << 1) | ((c & 3) >> 1)) | ((c & 1) << 8);
+  }
+  __device__ __forceinline__ int addr() const { return tp + ((((e & 7) ^ ((R ^ C) & 7)) << 1) | (e >> 8)); }
+  __device__ __forceinline__ void step() {
+    if constexpr (ADV_R) {
+      tp += M::dR(R) << 4;
+      ++R;
+    } else {
+      tp += 16;
+      ++C;
+    }
+  }
+};
+template <int N, bool ADV_R>
+struct KW<GM<N>, ADV_R> {
+  int tp;
+  __device__ __forceinline__ void init(int r, int c) { tp = r * N + c; }
+  __device__ __forceinline__ int addr() const { return tp; }
+  __device__ __forceinline__ void step() { tp += ADV_R ? 4 * N : 4; }
 };
 
 // A block view over a tiled matrix: element (i, j) of the view.
@@ -61,6 +104,8 @@ struct GM {
 // triangle (the reference's gather, verify.py:254-261).
 template <class M, bool TR, bool SY>
 struct TV {
+  using Mat = M;
+  static constexpr bool tr = TR, sy = SY;
   double* base;
   int r0, c0;
   __device__ __forceinline__ int off(int i, int j) const {
@@ -85,6 +130,71 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Operand streams along k for the DMMA loop.  A: element (i, k), B: (k, j).
+// Symmetric gathers (Lyapunov X_00 / X_11) pick, per lane and step, between
+// the upper element and its mirror.
+template <class AV>
+struct AStream {
+  KW<typename AV::Mat, AV::tr> w;
+  KW<typename AV::Mat, !AV::tr> wm;  // mirror walker (SY only)
+  int i_abs, k_abs;
+  __device__ __forceinline__ void init(const AV& v, int i) {
+    const int t = lane_id() & 3;
+    if constexpr (AV::sy) {
+      i_abs = v.r0 + i;
+      k_abs = v.c0 + t;
+      w.init(v.r0 + i, v.c0 + t);   // upper element (i, k): advance C
+      wm.init(v.c0 + t, v.r0 + i);  // mirror (k, i): advance R
+    } else if constexpr (AV::tr) {
+      w.init(v.r0 + t, v.c0 + i);
+    } else {
+      w.init(v.r0 + i, v.c0 + t);
+    }
+  }
+  __device__ __forceinline__ double load(const double* base) const {
+    if constexpr (AV::sy) return base[(i_abs <= k_abs) ? w.addr() : wm.addr()];
+    else return base[w.addr()];
+  }
+  __device__ __forceinline__ void step() {
+    w.step();
+    if constexpr (AV::sy) {
+      wm.step();
+      k_abs += 4;
+    }
+  }
+};
+
+template <class BV>
+struct BStream {
+  KW<typename BV::Mat, !BV::tr> w;
+  KW<typename BV::Mat, BV::tr> wm;
+  int j_abs, k_abs;
+  __device__ __forceinline__ void init(const BV& v, int j) {
+    const int t = lane_id() & 3;
+    if constexpr (BV::sy) {
+      j_abs = v.c0 + j;
+      k_abs = v.r0 + t;
+      w.init(v.r0 + t, v.c0 + j);   // upper element (k, j): advance R
+      wm.init(v.c0 + j, v.r0 + t);  // mirror (j, k): advance C
+    } else if constexpr (BV::tr) {
+      w.init(v.r0 + j, v.c0 + t);
+    } else {
+      w.init(v.r0 + t, v.c0 + j);
+    }
+  }
+  __device__ __forceinline__ double load(const double* base) const {
+    if constexpr (BV::sy) return base[(k_abs <= j_abs) ? w.addr() : wm.addr()];
+    else return base[w.addr()];
+  }
+  __device__ __forceinline__ void step() {
+    w.step();
+    if constexpr (BV::sy) {
+      wm.step();
+      k_abs += 4;
+    }
+  }
+};
+
 // ----------------------------------------------------------------------------
 // GEMM_update on the DMMA path: O(m x q) += sgn * A(m x p) B(p x q).
 // 16x16 warp blocks of 2x2 m8n8k4 tiles; m, p, q multiples of 4; partial
@@ -98,34 +208,46 @@ __device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int
   for (int i0 = 0; i0 < m; i0 += 16) {
     for (int j0 = 0; j0 < q; j0 += 16) {
       if (UP && i0 >= j0 + 16) continue;
-      // sub-tile validity (warp-uniform)
       const bool vi1 = i0 + 8 < m, vj1 = j0 + 8 < q;
       const bool v00 = !(UP && i0 >= j0 + 8);
       const bool v01 = vj1;
       const bool v10 = vi1 && !(UP && i0 + 8 >= j0 + 8);
       const bool v11 = vi1 && vj1 && !(UP && i0 + 8 >= j0 + 16);
-      // clamp rows/cols of partial 8-tiles to valid ones (results discarded)
       const int ra0 = i0 + ((i0 + g < m) ? g : (g & 3));
-      const int ra1 = i0 + 8 + ((i0 + 8 + g < m) ? g : (g & 3));
+      const int ra1 = vi1 ? i0 + 8 + ((i0 + 8 + g < m) ? g : (g & 3)) : ra0;
       const int cb0 = j0 + ((j0 + g < q) ? g : (g & 3));
-      const int cb1 = j0 + 8 + ((j0 + 8 + g < q) ? g : (g & 3));
+      const int cb1 = vj1 ? j0 + 8 + ((j0 + 8 + g < q) ? g : (g & 3)) : cb0;
+      AStream<AV> a0s, a1s;
+      BStream<BV> b0s, b1s;
+      a0s.init(A, ra0);
+      a1s.init(A, ra1);
+      b0s.init(Bm, cb0);
+      b1s.init(Bm, cb1);
       double c00a = 0, c00b = 0, c01a = 0, c01b = 0, c10a = 0, c10b = 0, c11a = 0, c11b = 0;
-#pragma unroll 2
       for (int k0 = 0; k0 < p; k0 += 4) {
-        const double a0 = A.at(ra0, k0 + t);
-        const double b0 = Bm.at(k0 + t, cb0);
-        const double a1 = vi1 ? A.at(ra1, k0 + t) : 0.0;
-        const double b1 = vj1 ? Bm.at(k0 + t, cb1) : 0.0;
+        const double a0 = a0s.load(A.base);
+        const double b0 = b0s.load(Bm.base);
+        const double a1 = a1s.load(A.base);
+        const double b1 = b1s.load(Bm.base);
         if (v00) dmma(c00a, c00b, a0, b0);
         if (v01) dmma(c01a, c01b, a0, b1);
         if (v10) dmma(c10a, c10b, a1, b0);
         if (v11) dmma(c11a, c11b, a1, b1);
+        a0s.step();
+        a1s.step();
+        b0s.step();
+        b1s.step();
       }
-      // write back: lane holds C[g][2t], C[g][2t+1] of each 8x8 tile
       auto wb = [&](int ib, int jb, double x0, double x1) {
         const int i = ib + g, j = jb + 2 * t;
-        if (i < m && j < q && (!UP || i <= j)) O.ref(i, j) = fma(sgn, x0, O.at(i, j));
-        if (i < m && j + 1 < q && (!UP || i <= j + 1)) O.ref(i, j + 1) = fma(sgn, x1, O.at(i, j + 1));
+        if (i < m && j < q && (!UP || i <= j)) {
+          double& o0 = O.ref(i, j);
+          o0 = fma(sgn, x0, o0);
+        }
+        if (i < m && j + 1 < q && (!UP || i <= j + 1)) {
+          double& o1 = O.ref(i, j + 1);
+          o1 = fma(sgn, x1, o1);
+        }
       };
       if (v00) wb(i0, j0, c00a, c00b);
       if (v01) wb(i0, j0 + 8, c01a, c01b);
@@ -137,34 +259,37 @@ __device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int
 
 // ----------------------------------------------------------------------------
 // TRSM_left_transposed: T W := W, T logically lower (m x m)  [kernels.py:47-60]
-// lanes own columns; forward substitution with broadcast coefficients.
 // ----------------------------------------------------------------------------
+// general m (Cholesky v0: coefficient X_00^T, m = kb): lanes own columns.
 template <class TVt, class WV>
 __device__ __forceinline__ void trsm(const TVt& Tm, const WV& W, int m, int q) {
   const int lane = lane_id();
   for (int j = lane; j < q; j += 32) {
     for (int i = 0; i < m; ++i) {
-      double s = 0.0;
-      for (int l = 0; l < i; ++l) s = fma(Tm.at(i, l), W.at(l, j), s);
-      W.ref(i, j) = (W.at(i, j) - s) / Tm.at(i, i);
+      double s = W.at(i, j);
+      for (int l = 0; l < i; ++l) s = fma(-Tm.at(i, l), W.at(l, j), s);
+      W.ref(i, j) = s / Tm.at(i, i);
     }
   }
 }
 
-// specialised for compile-time m = B <= 16: column in registers
+// compile-time m = B <= 16: column in registers, reciprocal pivots.
 template <int B, class TVt, class WV>
 __device__ __forceinline__ void trsm_b(const TVt& Tm, const WV& W, int q) {
   const int lane = lane_id();
+  double rd[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) rd[i] = 1.0 / Tm.at(i, i);
   for (int j = lane; j < q; j += 32) {
     double w[B];
 #pragma unroll
     for (int i = 0; i < B; ++i) w[i] = W.at(i, j);
 #pragma unroll
     for (int i = 0; i < B; ++i) {
-      double s = 0.0;
+      double s = w[i];
 #pragma unroll
-      for (int l = 0; l < i; ++l) s = fma(Tm.at(i, l), w[l], s);
-      w[i] = (w[i] - s) / Tm.at(i, i);
+      for (int l = 0; l < i; ++l) s = fma(-Tm.at(i, l), w[l], s);
+      w[i] = s * rd[i];
     }
 #pragma unroll
     for (int i = 0; i < B; ++i) W.ref(i, j) = w[i];
@@ -186,9 +311,9 @@ __device__ __forceinline__ void chol_leaf(const XV& W, int base, int* flag) {
   for (int i = 0; i < B; ++i) {
     const double piv = __shfl_sync(0xffffffffu, col[i], i);
     if (lane == 0 && piv <= 0.0 && *flag == 0) *flag = base + i + 1;
-    const double d = sqrt(piv);
-    if (j == i) col[i] = d;
-    else if (j > i) col[i] = col[i] / d;
+    const double rs = rsqrt(piv);
+    if (j == i) col[i] = piv * rs;
+    else if (j > i) col[i] = col[i] * rs;
 #pragma unroll
     for (int r = i + 1; r < B; ++r) {
       const double xir = __shfl_sync(0xffffffffu, col[i], r);
@@ -250,7 +375,6 @@ __device__ __forceinline__ void sylv(const LV& Lv, const UV& Uv, const WV& W, in
     for (int t = ilo + lane; t <= ihi; t += 32) sylv_tile(Lv, Uv, W, 4 * t, 4 * (d - t));
     if (d == TI + TJ - 2) break;
     __syncwarp();
-    // contributions of anti-diagonal d: units = (target tile, row a)
     const int units = TI * TJ * 4;
     for (int u = lane; u < units; u += 32) {
       const int tile = u >> 2, a = u & 3;
@@ -339,6 +463,7 @@ struct EqT;
 template <int N>
 struct EqT<0, N> {  // cholesky: X upper
   static constexpr int T = N / 4;
+  static constexpr bool STAGE = true;
   using M0 = TM<T, UPPER>;
   using M1 = M0;
   using M2 = M0;
@@ -348,6 +473,7 @@ struct EqT<0, N> {  // cholesky: X upper
 template <int N>
 struct EqT<1, N> {  // lyapunov: X upper (symmetric), L lower
   static constexpr int T = N / 4;
+  static constexpr bool STAGE = true;
   using M0 = TM<T, UPPER>;
   using M1 = TM<T, LOWER>;
   using M2 = M1;
@@ -357,7 +483,7 @@ struct EqT<1, N> {  // lyapunov: X upper (symmetric), L lower
 template <int N>
 struct EqT<2, N> {  // sylvester: X dense, L lower, U upper (global if too big)
   static constexpr int T = N / 4;
-  static constexpr bool STAGE = (T * T + T * (T + 1)) * 128 <= 227 * 1024;
+  static constexpr bool STAGE = (T * T + T * (T + 1)) * 128 <= 220 * 1024;
   using M0 = TM<T, DENSE>;
   using M1 = typename std::conditional<STAGE, TM<T, LOWER>, GM<N>>::type;
   using M2 = typename std::conditional<STAGE, TM<T, UPPER>, GM<N>>::type;
@@ -448,29 +574,35 @@ __device__ __forceinline__ void run_variant(Var<S...>, const Slot& s, int* flag)
 }
 
 // ----------------------------------------------------------------------------
-// global <-> tiled shared memory, one warp per problem
-// ----------------------------------------------------------------------------
+// global -> tiled shared memory (cp.async, 16 B chunks), one warp per problem
 // part: 0 = all tiles, 1 = upper tiles (C >= R), 2 = lower tiles (C <= R)
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NLEFT>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(NLEFT) : "memory");
+}
+
 template <class M, int N, int PART>
-__device__ __forceinline__ void load_tiles(double* dst, const double* __restrict__ src) {
+__device__ __forceinline__ void load_tiles_async(double* dst, const double* __restrict__ src) {
   constexpr int T = N / 4;
   const int lane = lane_id();
-  // unit = (R, rr, C): 4 consecutive doubles of one tile row
-  constexpr int UNITS = T * 4 * T;
+  // unit = (R, rr, C, half): 16 consecutive bytes of one tile row
+  constexpr int UNITS = T * 4 * T * 2;
   for (int u = lane; u < UNITS; u += 32) {
-    const int C = u % T;
-    const int rr = (u / T) & 3;
-    const int R = u / (4 * T);
+    const int h = u & 1;
+    const int C = (u >> 1) % T;
+    const int rr = ((u >> 1) / T) & 3;
+    const int R = (u >> 1) / (4 * T);
     if (PART == 1 && C < R) continue;
     if (PART == 2 && C > R) continue;
-    const int r = 4 * R + rr, c = 4 * C;
-    const double2* gp = reinterpret_cast<const double2*>(src + r * N + c);
-    const double2 v0 = __ldg(gp), v1 = __ldg(gp + 1);
-    double* tp = dst + (M::tidx(R, C) << 4);
-    const int key = (R ^ C) & 7;
-    const int ch0 = ((rr << 1) ^ key) & 7, ch1 = (((rr << 1) | 1) ^ key) & 7;
-    *reinterpret_cast<double2*>(tp + (ch0 << 1)) = v0;
-    *reinterpret_cast<double2*>(tp + (ch1 << 1)) = v1;
+    const int r = 4 * R + rr, c = 4 * C + 2 * h;
+    double* tp = dst + (M::tidx(R, C) << 4) + swz(r, c, (R ^ C) & 7);
+    cp_async16(tp, src + r * N + c);
   }
 }
 
@@ -488,23 +620,44 @@ __device__ __forceinline__ bool store_x(double* __restrict__ dst, const double* 
     const int r = 4 * R + rr, c = 4 * C;
     double v[4];
     if constexpr (EQ == 2) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = xs[M::off(r, c + e)];
+      const double2 p0 = *reinterpret_cast<const double2*>(xs + M::off(r, c));
+      const double2 p1 = *reinterpret_cast<const double2*>(xs + M::off(r, c + 2));
+      v[0] = p0.x;
+      v[1] = p0.y;
+      v[2] = p1.x;
+      v[3] = p1.y;
     } else if constexpr (EQ == 0) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = (c + e >= r) ? xs[M::off(r, c + e)] : 0.0;
+      if (C < R) {
+        v[0] = v[1] = v[2] = v[3] = 0.0;
+      } else {
+        const double2 p0 = *reinterpret_cast<const double2*>(xs + M::off(r, c));
+        const double2 p1 = *reinterpret_cast<const double2*>(xs + M::off(r, c + 2));
+        v[0] = (c >= r) ? p0.x : 0.0;
+        v[1] = (c + 1 >= r) ? p0.y : 0.0;
+        v[2] = (c + 2 >= r) ? p1.x : 0.0;
+        v[3] = (c + 3 >= r) ? p1.y : 0.0;
+      }
     } else {
+      if (C > R) {
+        const double2 p0 = *reinterpret_cast<const double2*>(xs + M::off(r, c));
+        const double2 p1 = *reinterpret_cast<const double2*>(xs + M::off(r, c + 2));
+        v[0] = p0.x;
+        v[1] = p0.y;
+        v[2] = p1.x;
+        v[3] = p1.y;
+      } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int cc = c + e;
-        v[e] = (cc >= r) ? xs[M::off(r, cc)] : xs[M::off(cc, r)];
+        for (int e = 0; e < 4; ++e) {
+          const int cc = c + e;
+          v[e] = (cc >= r) ? xs[M::off(r, cc)] : xs[M::off(cc, r)];
+        }
       }
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) finite = finite && isfinite(v[e]);
     double2* gp = reinterpret_cast<double2*>(dst + r * N + c);
-    gp[0] = make_double2(v[0], v[1]);
-    gp[1] = make_double2(v[2], v[3]);
+    __stcs(gp, make_double2(v[0], v[1]));
+    __stcs(gp + 1, make_double2(v[2], v[3]));
   }
   return finite;
 }
@@ -513,11 +666,33 @@ template <int EQ, int N>
 struct WPolicy {
   using E = EqT<EQ, N>;
   static constexpr int SLOT = E::SLOT;  // doubles per problem
-  // warps (= problem slots) per CTA: as many as fit in ~220 KB, at most 16
-  static constexpr int FIT = (220 * 1024) / (SLOT * 8);
+  static constexpr int BUDGET = 220 * 1024;
+  // double-buffer (prefetch the next problem) when that still leaves >= 6 warps
+  static constexpr int FIT2 = BUDGET / (2 * SLOT * 8);
+  static constexpr int DB = FIT2 >= 6 ? 2 : 1;
+  static constexpr int FIT = BUDGET / (DB * SLOT * 8);
   static constexpr int WARPS = FIT < 1 ? 1 : (FIT > 16 ? 16 : FIT);
-  static constexpr size_t SMEM = (size_t)WARPS * SLOT * 8;
+  static constexpr size_t SMEM = (size_t)WARPS * DB * SLOT * 8;
 };
+
+template <int EQ, int N>
+__device__ __forceinline__ void issue_loads(const Slot& s, const double* in0, const double* in1, const double* in2,
+                                            long long off) {
+  using E = EqT<EQ, N>;
+  if constexpr (EQ == 0) {
+    load_tiles_async<typename E::M0, N, 1>(s.p[0], in0 + off);
+  } else if constexpr (EQ == 1) {
+    load_tiles_async<typename E::M1, N, 2>(s.p[1], in0 + off);
+    load_tiles_async<typename E::M0, N, 1>(s.p[0], in1 + off);
+  } else {
+    if constexpr (E::STAGE) {
+      load_tiles_async<typename E::M1, N, 2>(s.p[1], in0 + off);
+      load_tiles_async<typename E::M2, N, 1>(s.p[2], in1 + off);
+    }
+    load_tiles_async<typename E::M0, N, 0>(s.p[0], in2 + off);
+  }
+  cp_async_commit();
+}
 
 template <int EQ, int N, int B, class VAR>
 __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
@@ -528,31 +703,38 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
-  double* base = smem + (size_t)warp * P::SLOT;
-  Slot s;
-  s.p[0] = base;
-  s.p[1] = base + E::M0::DOUBLES;
-  s.p[2] = (EQ == 2) ? base + E::M0::DOUBLES + E::M1::DOUBLES : s.p[1];
+  auto slot_at = [&](int d) {
+    Slot sl;
+    double* base = smem + ((size_t)warp * P::DB + (d % P::DB)) * P::SLOT;
+    sl.p[0] = base;
+    sl.p[1] = base + E::M0::DOUBLES;
+    sl.p[2] = (EQ == 2) ? base + E::M0::DOUBLES + E::M1::DOUBLES : sl.p[1];
+    return sl;
+  };
   constexpr long long NN = (long long)N * N;
   const long long stride = (long long)gridDim.x * P::WARPS;
-  for (long long prob = (long long)blockIdx.x * P::WARPS + warp; prob < batch; prob += stride) {
+  long long prob = (long long)blockIdx.x * P::WARPS + warp;
+  if (prob < batch) issue_loads<EQ, N>(slot_at(0), in0, in1, in2, prob * NN);
+  int cur = 0;
+  for (; prob < batch; prob += stride) {
     const long long off = prob * NN;
-    if constexpr (EQ == 0) {
-      load_tiles<typename E::M0, N, 1>(s.p[0], in0 + off);
-    } else if constexpr (EQ == 1) {
-      load_tiles<typename E::M1, N, 2>(s.p[1], in0 + off);
-      load_tiles<typename E::M0, N, 1>(s.p[0], in1 + off);
-    } else {
-      if constexpr (E::STAGE) {
-        load_tiles<typename E::M1, N, 2>(s.p[1], in0 + off);
-        load_tiles<typename E::M2, N, 1>(s.p[2], in1 + off);
+    const long long nxt = prob + stride;
+    Slot s = slot_at(cur);
+    if constexpr (P::DB == 2) {
+      if (nxt < batch) {
+        issue_loads<EQ, N>(slot_at(cur ^ 1), in0, in1, in2, nxt * NN);
+        cp_async_wait<1>();
       } else {
-        s.p[1] = const_cast<double*>(in0) + off;
-        s.p[2] = const_cast<double*>(in1) + off;
+        cp_async_wait<0>();
       }
-      load_tiles<typename E::M0, N, 0>(s.p[0], in2 + off);
+    } else {
+      cp_async_wait<0>();
     }
     __syncwarp();
+    if constexpr (EQ == 2 && !E::STAGE) {
+      s.p[1] = const_cast<double*>(in0) + off;
+      s.p[2] = const_cast<double*>(in1) + off;
+    }
     int flag = 0;
     run_variant<EQ, N, B>(VAR{}, s, &flag);
     const bool fin = store_x<EQ, typename E::M0, N>(X + off, s.p[0]);
@@ -560,6 +742,11 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
     flag = __shfl_sync(0xffffffffu, flag, 0);
     if (info && lane == 0) info[prob] = flag ? flag : (allfin ? 0 : -1);
     __syncwarp();
+    if constexpr (P::DB == 1) {
+      if (nxt < batch) issue_loads<EQ, N>(slot_at(0), in0, in1, in2, nxt * NN);
+    } else {
+      cur ^= 1;
+    }
   }
 }
 

@@ -11,6 +11,7 @@
 #include "inst_index.h"
 #include "lagen_b200.h"
 #include "registry.cuh"
+#include "registry_col.cuh"
 #include "registry_warp.cuh"
 #include "variants_table.h"
 
@@ -33,6 +34,16 @@ const WarpEntry* find_warp(int eq, int n, int b, int variant) {
   if (eq < 0 || eq > 2 || variant < 0) return nullptr;
   for (int p = 0; p < kWarpParts; ++p) {
     const WarpTable& t = kWarpTables[eq][p];
+    for (int i = 0; i < *t.n; ++i)
+      if (t.e[i].n == n && t.e[i].b == b && t.e[i].variant == variant) return &t.e[i];
+  }
+  return nullptr;
+}
+
+const ColEntry* find_col(int eq, int n, int b, int variant) {
+  if (eq != 0 || variant < 0) return nullptr;
+  for (int p = 0; p < kColParts; ++p) {
+    const ColTable& t = kColTables[p];
     for (int i = 0; i < *t.n; ++i)
       if (t.e[i].n == n && t.e[i].b == b && t.e[i].variant == variant) return &t.e[i];
   }
@@ -194,6 +205,15 @@ int lagen_b200_geometry(int eq, int n, int b, int* g, int* p, int* threads, int*
 
 int lagen_b200_warp_supported(int eq, int n, int b, int variant) { return find_warp(eq, n, b, variant) ? 1 : 0; }
 
+int lagen_b200_engine_supported(int eq, int n, int b, int variant, int engine) {
+  switch (engine) {
+    case LAGEN_ENGINE_GENERIC: return find_entry(eq, n, b) ? 1 : 0;
+    case LAGEN_ENGINE_WARP: return find_warp(eq, n, b, variant) ? 1 : 0;
+    case LAGEN_ENGINE_COLUMN: return find_col(eq, n, b, variant) ? 1 : 0;
+  }
+  return 0;
+}
+
 int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                        const double* const* inputs, double* X, int* info, void* stream) {
   return lagen_b200_execute_engine(eq, stmts, nstmts, n, b, batch, inputs, X, info, stream, LAGEN_ENGINE_AUTO);
@@ -201,7 +221,7 @@ int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b
 
 int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                               const double* const* inputs, double* X, int* info, void* stream, int engine) {
-  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_WARP) return fail(LAGEN_EINVAL, "unknown engine");
+  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_COLUMN) return fail(LAGEN_EINVAL, "unknown engine");
   int rc = check_common(eq, n, b, batch);
   if (rc) return rc;
   rc = validate(eq, stmts, nstmts);
@@ -218,15 +238,19 @@ int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n
   a.X = X;
   a.info = info;
   a.batch = batch;
-  const WarpEntry* w = nullptr;
+  LaunchFn fn = find_entry(eq, n, b)->launch;
   if (engine != LAGEN_ENGINE_GENERIC) {
     const int v = match_builtin(eq, stmts, nstmts);
-    w = find_warp(eq, n, b, v);
-    if (!w && engine == LAGEN_ENGINE_WARP)
+    const ColEntry* c = (engine == LAGEN_ENGINE_AUTO || engine == LAGEN_ENGINE_COLUMN) ? find_col(eq, n, b, v) : nullptr;
+    const WarpEntry* w = (engine == LAGEN_ENGINE_AUTO || engine == LAGEN_ENGINE_WARP) ? find_warp(eq, n, b, v) : nullptr;
+    if (engine == LAGEN_ENGINE_COLUMN && !c)
+      return fail(LAGEN_EUNSUPPORTED, "no column-engine instance for this (variant, n, b)");
+    if (engine == LAGEN_ENGINE_WARP && !w)
       return fail(LAGEN_EUNSUPPORTED, "no warp-engine instance for this (variant, n, b)");
+    if (c) fn = c->launch;
+    else if (w) fn = w->launch;
   }
-  cudaError_t err = w ? w->launch(a, static_cast<cudaStream_t>(stream))
-                      : find_entry(eq, n, b)->launch(a, static_cast<cudaStream_t>(stream));
+  cudaError_t err = fn(a, static_cast<cudaStream_t>(stream));
   if (err != cudaSuccess) return cuda_fail(err, "solve launch");
   return LAGEN_OK;
 }

@@ -57,8 +57,8 @@ def test_golden_reference_vectors(eq):
         groups.setdefault((e["n"], e["variant"], e["b"]), []).append(e)
     from paper_1906_08613_b200 import _lib
     for (n, v, b), es in groups.items():
-      for engine in ("generic", "warp"):
-        if engine == "warp" and not _lib.lib.lagen_b200_warp_supported(EQ_CODES[eq], n, b, v):
+      for engine in ("generic", "warp", "column"):
+        if not _lib.engine_supported(EQ_CODES[eq], n, b, v, engine):
             continue
         ins = [np.stack([d[f"in_{e['case']}_{n}_{nm}"] for e in es]) for nm in EQ_INPUTS[eq]]
         X, info = executor.solve(eq, to_dev(ins), variant=v, b=b, engine=engine)
@@ -89,9 +89,8 @@ def test_every_variant_vs_oracle(eq, n, oracle_mod):
     assert (ref_info == 0).all()
     res_tol = 10 * n * EPS
     from paper_1906_08613_b200 import _lib
-    runs = [(v, b, "generic") for v in vs for b in default_blocks(n)]
-    runs += [(v, b, "warp") for v in vs for b in default_blocks(n)
-             if _lib.lib.lagen_b200_warp_supported(EQ_CODES[eq], n, b, v.index)]
+    runs = [(v, b, e) for e in ("generic", "warp", "column") for v in vs for b in default_blocks(n)
+            if _lib.engine_supported(EQ_CODES[eq], n, b, v.index, e)]
     for v, b, engine in runs:
         if True:
             X, info = executor.solve(eq, ins_d, variant=v.index, b=b, engine=engine)

@@ -55,9 +55,9 @@ def main():
             rows = []
             ref_X = None
             from paper_1906_08613_b200 import _lib
-            cands = [(v, b, "generic") for v in builtin_variants(eq) for b in default_blocks(n)]
-            cands += [(v, b, "warp") for v in builtin_variants(eq) for b in default_blocks(n)
-                      if _lib.lib.lagen_b200_warp_supported(_lib_eq(eq), n, b, v.index)]
+            cands = [(v, b, e) for e in ("generic", "warp", "column")
+                     for v in builtin_variants(eq) for b in default_blocks(n)
+                     if _lib.engine_supported(_lib_eq(eq), n, b, v.index, e)]
             if args.engines != "all":
                 cands = [c for c in cands if c[2] in args.engines.split(",")]
             for v, b, engine in cands:
@@ -86,6 +86,8 @@ def main():
                     rows.append({"variant": v.index, "b": b, "engine": engine, "ms": round(ms, 5), "ok": ok})
                     del plan
             good = [r for r in rows if r["ok"]]
+            if not good:
+                continue
             best = min(good, key=lambda r: (r["ms"], r["variant"], r["b"]))
             table[eq][str(n)] = {"variant": best["variant"], "b": best["b"], "engine": best["engine"],
                                  "ms": best["ms"]}
