@@ -36,7 +36,8 @@ struct ColPolicy {
   static constexpr int CPL = N <= 32 ? 1 : 2;                            // columns per lane
   static constexpr int GPW = 32 / W;                                     // problems per warp
   static constexpr int WARPS = N <= 32 ? 8 : 4;                          // warps per CTA
-  static constexpr int PUB_LD = 17;                       // publish buffer: <= 16 rows per column
+  static constexpr int MINB = N <= 32 ? 2 : 1;  // >= 16 warps/SM for n <= 32 (<= 128 regs)
+  static constexpr int PUB_LD = 18;  // publish buffer: <= 16 rows per column; even -> LDS.128 pairs
   static constexpr int PUB = PUB_LD * (N < 32 ? N : 32);  // <= 32 columns per publish
   static constexpr int SMEM = WARPS * GPW * PUB * 8;
 };
@@ -86,7 +87,7 @@ __device__ __forceinline__ void sfor(F&& f) {
 }
 
 template <int N, int B, int VARIANT>
-__global__ void __launch_bounds__(ColPolicy<N>::WARPS * 32)
+__global__ void __launch_bounds__(ColPolicy<N>::WARPS * 32, ColPolicy<N>::MINB)
     chol_col_kernel(const double* __restrict__ A, double* __restrict__ X, int* __restrict__ info, long long batch) {
   using Pol = ColPolicy<N>;
   using K = Chol<N, B, VARIANT>;
@@ -158,14 +159,15 @@ __global__ void __launch_bounds__(ColPolicy<N>::WARPS * 32)
           sfor<0, nr>([&](auto iI) {
             constexpr int r = ro + decltype(iI)::value;
             // X(l, r) for l in [lo, hi): column r of the published block
-            double acc0 = 0.0, acc1 = 0.0;
+            double acc0 = 0.0, acc1 = 0.0, acc0b = 0.0, acc1b = 0.0;
             sfor<0, (hi - lo + 1) / 2>([&](auto pI) {
               constexpr int l = lo + 2 * decltype(pI)::value;
               const double* src = pub + (r - ro) * LD + (l - lo);
               double xr0, xr1;
               if constexpr (l + 1 < hi) {
-                xr0 = src[0];
-                xr1 = src[1];
+                const double2 pr = *reinterpret_cast<const double2*>(src);
+                xr0 = pr.x;
+                xr1 = pr.y;
               } else {
                 xr0 = src[0];
                 xr1 = 0.0;
@@ -174,8 +176,9 @@ __global__ void __launch_bounds__(ColPolicy<N>::WARPS * 32)
                 constexpr int s = decltype(sI)::value;
                 if constexpr (s == 1 || (l < 32 && (l + 1 < 32 || l + 1 >= hi))) {
                   double& acc = s == 0 ? acc0 : acc1;
+                  double& accb = s == 0 ? acc0b : acc1b;
                   acc = fma(xr0, K::template cv<l, s>(cs), acc);
-                  if constexpr (l + 1 < hi) acc = fma(xr1, K::template cv<(l + 1 < hi ? l + 1 : l), s>(cs), acc);
+                  if constexpr (l + 1 < hi) accb = fma(xr1, K::template cv<(l + 1 < hi ? l + 1 : l), s>(cs), accb);
                 }
               });
             });
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(ColPolicy<N>::WARPS * 32)
               constexpr int s = decltype(sI)::value;
               if constexpr (s == 1 || r < 32) {
                 const int j = jj[s];
-                const double acc = s == 0 ? acc0 : acc1;
+                const double acc = s == 0 ? acc0 + acc0b : acc1 + acc1b;
                 if (j >= cmin && j < cmax && (!up || r <= j)) K::template cv<r, s>(cs) -= acc;
               }
             });
@@ -244,6 +247,80 @@ __global__ void __launch_bounds__(ColPolicy<N>::WARPS * 32)
         }
       };
 
+      // B <= 8: CHOL leaf computed redundantly by every lane of the group from
+      // the published diagonal block (no shuffles on the pivot chain), then
+      // the TRSM of block row 1 uses the factor and its reciprocal pivots
+      // (rsqrt) straight from registers.
+      auto leaf_trsm_reg = [&]() {
+        publish(std::integral_constant<int, s1>{}, std::integral_constant<int, s2>{},
+                std::integral_constant<int, s1>{}, std::integral_constant<int, s2>{});
+        double t[B][B];
+        double rs[B];
+        sfor<0, B>([&](auto cI) {
+          constexpr int c = decltype(cI)::value;
+          sfor<0, c + 1>([&](auto rI) {
+            constexpr int r = decltype(rI)::value;
+            t[r][c] = pub[c * LD + r];
+          });
+        });
+        sfor<0, B>([&](auto iI) {
+          constexpr int i = decltype(iI)::value;
+          const double piv = t[i][i];
+          if (gl == 0 && piv <= 0.0 && flag == 0) flag = s1 + i + 1;
+          rs[i] = rsqrt(piv);
+          t[i][i] = piv * rs[i];
+          sfor<i + 1, B>([&](auto cI) {
+            constexpr int c = decltype(cI)::value;
+            t[i][c] *= rs[i];
+          });
+          sfor<i + 1, B>([&](auto rI) {
+            constexpr int r = decltype(rI)::value;
+            sfor<r, B>([&](auto cI) {
+              constexpr int c = decltype(cI)::value;
+              t[r][c] = fma(-t[i][r], t[i][c], t[r][c]);
+            });
+          });
+        });
+        // own column inside block 1 takes its factor column
+        sfor<0, CPL>([&](auto sI) {
+          constexpr int s = decltype(sI)::value;
+          const int j = jj[s];
+          sfor<0, B>([&](auto cI) {
+            constexpr int c = decltype(cI)::value;
+            if constexpr (s == 1 || s1 + c < 32) {
+              if (j == s1 + c) {
+                sfor<0, c + 1>([&](auto rI) {
+                  constexpr int r = decltype(rI)::value;
+                  K::template cv<s1 + r, s>(cs) = t[r][c];
+                });
+              }
+            }
+          });
+        });
+        // X12 := TRSM(X11^T, X12): T(i, l) = X(l, i) = t[l][i]
+        if constexpr (s2 < N) {
+          sfor<0, CPL>([&](auto sI) {
+            constexpr int s = decltype(sI)::value;
+            if constexpr (s == 1 || s2 <= 32) {
+              const int j = jj[s];
+              double w[B];
+              sfor<0, B>([&](auto iI) {
+                constexpr int i = decltype(iI)::value;
+                if constexpr (s == 1 || s1 + i < 32) {
+                  double v = K::template cv<s1 + i, s>(cs);
+                  sfor<0, i>([&](auto lI) {
+                    constexpr int l = decltype(lI)::value;
+                    v = fma(-t[l][i], w[l], v);
+                  });
+                  w[i] = v * rs[i];
+                  if (j >= s2 && j < N) K::template cv<s1 + i, s>(cs) = w[i];
+                }
+              });
+            }
+          });
+        }
+      };
+
       using I0 = std::integral_constant<int, 0>;
       using IS1 = std::integral_constant<int, s1>;
       using IS2 = std::integral_constant<int, s2>;
@@ -267,12 +344,18 @@ __global__ void __launch_bounds__(ColPolicy<N>::WARPS * 32)
             });
           }
         }
-        leaf();
-        trsm();
+        if constexpr (B <= 4 || (B <= 8 && CPL == 1)) leaf_trsm_reg();
+        else {
+          leaf();
+          trsm();
+        }
       } else {
         // v2: leaf, trsm, then X22 -= X12^T X12 (upper)
-        leaf();
-        trsm();
+        if constexpr (B <= 4 || (B <= 8 && CPL == 1)) leaf_trsm_reg();
+        else {
+          leaf();
+          trsm();
+        }
         if constexpr (s2 < N) {
           sfor<0, (N - s2 + 31) / 32>([&](auto cI) {
             constexpr int c0 = s2 + 32 * decltype(cI)::value;
