@@ -130,6 +130,18 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// A problem is owned by a group of WG warps (G = 32 * WG threads).
+struct Grp {
+  int rank;  // 0 .. G-1
+  int wig;   // warp in group
+  int id;    // group index in the CTA (named barrier id - 1)
+};
+template <int WG>
+__device__ __forceinline__ void gsync(const Grp& g) {
+  if constexpr (WG == 1) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(g.id + 1), "r"(WG * 32) : "memory");
+}
+
 // Operand streams along k for the DMMA loop.  A: element (i, k), B: (k, j).
 // Symmetric gathers (Lyapunov X_00 / X_11) pick, per lane and step, between
 // the upper element and its mirror.
@@ -201,12 +213,16 @@ struct BStream {
 // 8-row/col tiles read clamped (valid) rows and discard them on write.
 // UP: upper target (only i <= j written; tiles strictly below skipped).
 // ----------------------------------------------------------------------------
-template <bool UP, class OV, class AV, class BV>
-__device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int m, int p, int q, double sgn) {
+template <bool UP, int WG, class OV, class AV, class BV>
+__device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int m, int p, int q, double sgn,
+                                     const Grp& gr) {
   const int lane = lane_id();
   const int g = lane >> 2, t = lane & 3;
-  for (int i0 = 0; i0 < m; i0 += 16) {
-    for (int j0 = 0; j0 < q; j0 += 16) {
+  const int nbj = (q + 15) >> 4;
+  const int nblk = ((m + 15) >> 4) * nbj;
+  for (int bk = gr.wig; bk < nblk; bk += WG) {
+    {
+      const int i0 = (bk / nbj) << 4, j0 = (bk % nbj) << 4;
       if (UP && i0 >= j0 + 16) continue;
       const bool vi1 = i0 + 8 < m, vj1 = j0 + 8 < q;
       const bool v00 = !(UP && i0 >= j0 + 8);
@@ -261,10 +277,9 @@ __device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int
 // TRSM_left_transposed: T W := W, T logically lower (m x m)  [kernels.py:47-60]
 // ----------------------------------------------------------------------------
 // general m (Cholesky v0: coefficient X_00^T, m = kb): lanes own columns.
-template <class TVt, class WV>
-__device__ __forceinline__ void trsm(const TVt& Tm, const WV& W, int m, int q) {
-  const int lane = lane_id();
-  for (int j = lane; j < q; j += 32) {
+template <int WG, class TVt, class WV>
+__device__ __forceinline__ void trsm(const TVt& Tm, const WV& W, int m, int q, const Grp& gr) {
+  for (int j = gr.rank; j < q; j += 32 * WG) {
     for (int i = 0; i < m; ++i) {
       double s = W.at(i, j);
       for (int l = 0; l < i; ++l) s = fma(-Tm.at(i, l), W.at(l, j), s);
@@ -274,13 +289,13 @@ __device__ __forceinline__ void trsm(const TVt& Tm, const WV& W, int m, int q) {
 }
 
 // compile-time m = B <= 16: column in registers, reciprocal pivots.
-template <int B, class TVt, class WV>
-__device__ __forceinline__ void trsm_b(const TVt& Tm, const WV& W, int q) {
-  const int lane = lane_id();
+template <int B, int WG, class TVt, class WV>
+__device__ __forceinline__ void trsm_b(const TVt& Tm, const WV& W, int q, const Grp& gr) {
+  if (gr.rank >= q) return;
   double rd[B];
 #pragma unroll
   for (int i = 0; i < B; ++i) rd[i] = 1.0 / Tm.at(i, i);
-  for (int j = lane; j < q; j += 32) {
+  for (int j = gr.rank; j < q; j += 32 * WG) {
     double w[B];
 #pragma unroll
     for (int i = 0; i < B; ++i) w[i] = W.at(i, j);
@@ -341,6 +356,15 @@ __device__ __forceinline__ void sylv_tile(const LV& Lv, const UV& Uv, const WV& 
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) w[a][b] = W.at(i0 + a, j0 + b);
+  // reciprocal shifted pivots 1 / (l_aa + u_bb): 16 independent divisions
+  // off the substitution chain (<= 1 ulp from the reference's division)
+  double rp[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const double laa = Lv.at(i0 + a, i0 + a);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) rp[a][b] = 1.0 / (laa + Uv.at(j0 + b, j0 + b));
+  }
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
 #pragma unroll
@@ -350,13 +374,12 @@ __device__ __forceinline__ void sylv_tile(const LV& Lv, const UV& Uv, const WV& 
       for (int c = 0; c < b; ++c) acc = fma(w[a][c], Uv.at(j0 + c, j0 + b), acc);
       w[a][b] -= acc;
     }
-    const double ujj = Uv.at(j0 + b, j0 + b);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       double acc = 0.0;
 #pragma unroll
       for (int c = 0; c < a; ++c) acc = fma(Lv.at(i0 + a, i0 + c), w[c][b], acc);
-      w[a][b] = (w[a][b] - acc) / (Lv.at(i0 + a, i0 + a) + ujj);
+      w[a][b] = (w[a][b] - acc) * rp[a][b];
     }
   }
 #pragma unroll
@@ -365,18 +388,19 @@ __device__ __forceinline__ void sylv_tile(const LV& Lv, const UV& Uv, const WV& 
     for (int b = 0; b < 4; ++b) W.ref(i0 + a, j0 + b) = w[a][b];
 }
 
-template <class LV, class UV, class WV>
-__device__ __forceinline__ void sylv(const LV& Lv, const UV& Uv, const WV& W, int m, int q) {
-  const int lane = lane_id();
+template <int WG, class LV, class UV, class WV>
+__device__ __forceinline__ void sylv(const LV& Lv, const UV& Uv, const WV& W, int m, int q, const Grp& gr) {
+  const int lane = gr.rank;
+  constexpr int G = 32 * WG;
   const int TI = m >> 2, TJ = q >> 2;
   for (int d = 0; d <= TI + TJ - 2; ++d) {
     const int ilo = d - (TJ - 1) > 0 ? d - (TJ - 1) : 0;
     const int ihi = d < TI - 1 ? d : TI - 1;
-    for (int t = ilo + lane; t <= ihi; t += 32) sylv_tile(Lv, Uv, W, 4 * t, 4 * (d - t));
+    for (int t = ilo + lane; t <= ihi; t += G) sylv_tile(Lv, Uv, W, 4 * t, 4 * (d - t));
     if (d == TI + TJ - 2) break;
-    __syncwarp();
+    gsync<WG>(gr);
     const int units = TI * TJ * 4;
-    for (int u = lane; u < units; u += 32) {
+    for (int u = lane; u < units; u += G) {
       const int tile = u >> 2, a = u & 3;
       const int I2 = tile / TJ, J2 = tile - I2 * TJ;
       if (I2 + J2 <= d) continue;
@@ -409,7 +433,7 @@ __device__ __forceinline__ void sylv(const LV& Lv, const UV& Uv, const WV& W, in
         W.ref(i, j) -= s;
       }
     }
-    __syncwarp();
+    gsync<WG>(gr);
   }
 }
 
@@ -417,23 +441,24 @@ __device__ __forceinline__ void sylv(const LV& Lv, const UV& Uv, const WV& W, in
 // LYAP leaf (symmetric, upper stored) [kernels.py:113-130]: element
 // anti-diagonal wavefront, pull model; writes the upper triangle only.
 // ----------------------------------------------------------------------------
-template <class LV, class WV, class WSV>
-__device__ __forceinline__ void lyap(const LV& Lv, const WV& W, const WSV& Ws, int m) {
-  const int lane = lane_id();
+template <int WG, class LV, class WV, class WSV>
+__device__ __forceinline__ void lyap(const LV& Lv, const WV& W, const WSV& Ws, int m, const Grp& gr) {
+  const int lane = gr.rank;
   for (int d = 0; d <= 2 * (m - 1); ++d) {
     const int ilo = d - (m - 1) > 0 ? d - (m - 1) : 0;
     const int ihi = d >> 1;
-    for (int i = ilo + lane; i <= ihi; i += 32) {
+    for (int i = ilo + lane; i <= ihi; i += 32 * WG) {
       const int j = d - i;
+      const double rp = 1.0 / (Lv.at(i, i) + Lv.at(j, j));  // off the dot-product chain
       double acc = W.at(i, j);
       double d1 = 0.0, d2 = 0.0;
       for (int l = 0; l < i; ++l) d1 = fma(Lv.at(i, l), W.at(l, j), d1);
       for (int l = 0; l < j; ++l) d2 = fma(Ws.at(i, l), Lv.at(j, l), d2);
       acc -= d1;
       acc -= d2;
-      W.ref(i, j) = acc / (Lv.at(i, i) + Lv.at(j, j));
+      W.ref(i, j) = acc * rp;
     }
-    __syncwarp();
+    gsync<WG>(gr);
   }
 }
 
@@ -524,8 +549,8 @@ __device__ __forceinline__ TV<typename MatOf<E, Vw::op>::type, Vw::tr != 0, SY> 
   return v;
 }
 
-template <int EQ, int N, int B, class S>
-__device__ __forceinline__ void exec(const Slot& s, const Rep<N, B>& rp, int* flag) {
+template <int EQ, int N, int B, int WG, class S>
+__device__ __forceinline__ void exec(const Slot& s, const Rep<N, B>& rp, int* flag, const Grp& gr) {
   using E = EqT<EQ, N>;
   using O = typename S::out;
   const int m = rp.ex(O::r), q = rp.ex(O::c);
@@ -541,35 +566,35 @@ __device__ __forceinline__ void exec(const Slot& s, const Rep<N, B>& rp, int* fl
     constexpr bool SB = E::SYMX && Bv::op == 0 && Bv::r == Bv::c;
     const auto Av = mkv<E, A, SA>(s, rp.st(A::r), rp.st(A::c));
     const auto Bw = mkv<E, Bv, SB>(s, rp.st(Bv::r), rp.st(Bv::c));
-    gemm<UP>(Ov, Av, Bw, m, p, q, S::sign < 0 ? -1.0 : 1.0);
+    gemm<UP, WG>(Ov, Av, Bw, m, p, q, S::sign < 0 ? -1.0 : 1.0, gr);
   } else if constexpr (S::kind == K_CHOL) {
-    chol_leaf<B>(Ov, rp.st(O::r), flag);
+    if (gr.wig == 0) chol_leaf<B>(Ov, rp.st(O::r), flag);
   } else if constexpr (S::kind == K_TRSM) {
     using A = typename S::in0;
     const auto Tv = mkv<E, A, false>(s, rp.st(A::r), rp.st(A::c));
-    if constexpr (O::r == 1) trsm_b<B>(Tv, Ov, q);  // m == B
-    else trsm(Tv, Ov, m, q);
+    if constexpr (O::r == 1) trsm_b<B, WG>(Tv, Ov, q, gr);  // m == B
+    else trsm<WG>(Tv, Ov, m, q, gr);
   } else if constexpr (S::kind == K_SYLV) {
     using A = typename S::in0;
     using Bv = typename S::in1;
     const auto Lv = mkv<E, A, false>(s, rp.st(A::r), rp.st(A::c));
     const auto Uv = mkv<E, Bv, false>(s, rp.st(Bv::r), rp.st(Bv::c));
-    sylv(Lv, Uv, Ov, m, q);
+    sylv<WG>(Lv, Uv, Ov, m, q, gr);
   } else if constexpr (S::kind == K_LYAP) {
     using A = typename S::in0;
     const auto Lv = mkv<E, A, false>(s, rp.st(A::r), rp.st(A::c));
     const auto Ws = mkv<E, O, true>(s, rp.st(O::r), rp.st(O::c));
-    lyap(Lv, Ov, Ws, m);
+    lyap<WG>(Lv, Ov, Ws, m, gr);
   }
-  __syncwarp();
+  gsync<WG>(gr);
 }
 
-template <int EQ, int N, int B, class... S>
-__device__ __forceinline__ void run_variant(Var<S...>, const Slot& s, int* flag) {
+template <int EQ, int N, int B, int WG, class... S>
+__device__ __forceinline__ void run_variant(Var<S...>, const Slot& s, int* flag, const Grp& gr) {
 #pragma unroll 1
   for (int k = 0; k < N / B; ++k) {
     Rep<N, B> rp{k};
-    (exec<EQ, N, B, S>(s, rp, flag), ...);
+    (exec<EQ, N, B, WG, S>(s, rp, flag, gr), ...);
   }
 }
 
@@ -587,13 +612,12 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(NLEFT) : "memory");
 }
 
-template <class M, int N, int PART>
-__device__ __forceinline__ void load_tiles_async(double* dst, const double* __restrict__ src) {
+template <class M, int N, int PART, int G>
+__device__ __forceinline__ void load_tiles_async(double* dst, const double* __restrict__ src, int rank) {
   constexpr int T = N / 4;
-  const int lane = lane_id();
   // unit = (R, rr, C, half): 16 consecutive bytes of one tile row
   constexpr int UNITS = T * 4 * T * 2;
-  for (int u = lane; u < UNITS; u += 32) {
+  for (int u = rank; u < UNITS; u += G) {
     const int h = u & 1;
     const int C = (u >> 1) % T;
     const int rr = ((u >> 1) / T) & 3;
@@ -607,13 +631,12 @@ __device__ __forceinline__ void load_tiles_async(double* dst, const double* __re
 }
 
 // store all n^2 entries of X; EQ decides zeros (chol) / mirror (lyap)
-template <int EQ, class M, int N>
-__device__ __forceinline__ bool store_x(double* __restrict__ dst, const double* xs) {
+template <int EQ, class M, int N, int G>
+__device__ __forceinline__ bool store_x(double* __restrict__ dst, const double* xs, int rank) {
   constexpr int T = N / 4;
-  const int lane = lane_id();
   constexpr int UNITS = T * 4 * T;
   bool finite = true;
-  for (int u = lane; u < UNITS; u += 32) {
+  for (int u = rank; u < UNITS; u += G) {
     const int C = u % T;
     const int rr = (u / T) & 3;
     const int R = u / (4 * T);
@@ -667,54 +690,69 @@ struct WPolicy {
   using E = EqT<EQ, N>;
   static constexpr int SLOT = E::SLOT;  // doubles per problem
   static constexpr int BUDGET = 220 * 1024;
-  // double-buffer (prefetch the next problem) when that still leaves >= 6 warps
-  static constexpr int FIT2 = BUDGET / (2 * SLOT * 8);
-  static constexpr int DB = FIT2 >= 6 ? 2 : 1;
-  static constexpr int FIT = BUDGET / (DB * SLOT * 8);
-  static constexpr int WARPS = FIT < 1 ? 1 : (FIT > 16 ? 16 : FIT);
-  static constexpr size_t SMEM = (size_t)WARPS * DB * SLOT * 8;
+  static constexpr int TARGET_WARPS = 12;
+  // problem slots that fit single / double buffered
+  static constexpr int S1 = BUDGET / (SLOT * 8);
+  static constexpr int S2 = BUDGET / (2 * SLOT * 8);
+  // double-buffer (prefetch the next problem) when >= 6 problems still fit
+  static constexpr int DB = S2 >= 6 ? 2 : 1;
+  static constexpr int P0 = DB == 2 ? S2 : (S1 < 1 ? 1 : S1);
+  static constexpr int P = P0 > 16 ? 16 : (P0 > 15 && TARGET_WARPS > P0 ? 15 : P0);
+  // warps per problem: smallest power of two reaching TARGET_WARPS per CTA
+  static constexpr int WG = P >= TARGET_WARPS ? 1 : (2 * P >= TARGET_WARPS ? 2 : (4 * P >= TARGET_WARPS ? 4 : (8 * P >= TARGET_WARPS ? 8 : 16)));
+  static constexpr int WARPS = P * WG;
+  static constexpr size_t SMEM = (size_t)P * DB * SLOT * 8 + 2 * 16 * sizeof(int);
 };
 
-template <int EQ, int N>
+template <int EQ, int N, int G>
 __device__ __forceinline__ void issue_loads(const Slot& s, const double* in0, const double* in1, const double* in2,
-                                            long long off) {
+                                            long long off, int rank) {
   using E = EqT<EQ, N>;
   if constexpr (EQ == 0) {
-    load_tiles_async<typename E::M0, N, 1>(s.p[0], in0 + off);
+    load_tiles_async<typename E::M0, N, 1, G>(s.p[0], in0 + off, rank);
   } else if constexpr (EQ == 1) {
-    load_tiles_async<typename E::M1, N, 2>(s.p[1], in0 + off);
-    load_tiles_async<typename E::M0, N, 1>(s.p[0], in1 + off);
+    load_tiles_async<typename E::M1, N, 2, G>(s.p[1], in0 + off, rank);
+    load_tiles_async<typename E::M0, N, 1, G>(s.p[0], in1 + off, rank);
   } else {
     if constexpr (E::STAGE) {
-      load_tiles_async<typename E::M1, N, 2>(s.p[1], in0 + off);
-      load_tiles_async<typename E::M2, N, 1>(s.p[2], in1 + off);
+      load_tiles_async<typename E::M1, N, 2, G>(s.p[1], in0 + off, rank);
+      load_tiles_async<typename E::M2, N, 1, G>(s.p[2], in1 + off, rank);
     }
-    load_tiles_async<typename E::M0, N, 0>(s.p[0], in2 + off);
+    load_tiles_async<typename E::M0, N, 0, G>(s.p[0], in2 + off, rank);
   }
   cp_async_commit();
 }
 
+// CTA = P problem groups x WG warps; persistent over the batch; each group
+// prefetches its next problem (DB == 2) while solving the current one.
 template <int EQ, int N, int B, class VAR>
 __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
     warp_kernel(const double* __restrict__ in0, const double* __restrict__ in1, const double* __restrict__ in2,
                 double* __restrict__ X, int* __restrict__ info, long long batch) {
   using E = EqT<EQ, N>;
   using P = WPolicy<EQ, N>;
+  constexpr int WG = P::WG, G = WG * 32;
   extern __shared__ double smem[];
+  int* gflag = reinterpret_cast<int*>(smem + (size_t)P::P * P::DB * P::SLOT);
+  int* gbad = gflag + 16;
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
+  Grp gr;
+  gr.id = warp / WG;
+  gr.wig = warp % WG;
+  gr.rank = threadIdx.x % G;
   auto slot_at = [&](int d) {
     Slot sl;
-    double* base = smem + ((size_t)warp * P::DB + (d % P::DB)) * P::SLOT;
+    double* base = smem + ((size_t)gr.id * P::DB + (d % P::DB)) * P::SLOT;
     sl.p[0] = base;
     sl.p[1] = base + E::M0::DOUBLES;
     sl.p[2] = (EQ == 2) ? base + E::M0::DOUBLES + E::M1::DOUBLES : sl.p[1];
     return sl;
   };
   constexpr long long NN = (long long)N * N;
-  const long long stride = (long long)gridDim.x * P::WARPS;
-  long long prob = (long long)blockIdx.x * P::WARPS + warp;
-  if (prob < batch) issue_loads<EQ, N>(slot_at(0), in0, in1, in2, prob * NN);
+  const long long stride = (long long)gridDim.x * P::P;
+  long long prob = (long long)blockIdx.x * P::P + gr.id;
+  if (prob < batch) issue_loads<EQ, N, G>(slot_at(0), in0, in1, in2, prob * NN, gr.rank);
   int cur = 0;
   for (; prob < batch; prob += stride) {
     const long long off = prob * NN;
@@ -722,7 +760,7 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
     Slot s = slot_at(cur);
     if constexpr (P::DB == 2) {
       if (nxt < batch) {
-        issue_loads<EQ, N>(slot_at(cur ^ 1), in0, in1, in2, nxt * NN);
+        issue_loads<EQ, N, G>(slot_at(cur ^ 1), in0, in1, in2, nxt * NN, gr.rank);
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
@@ -730,20 +768,29 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
     } else {
       cp_async_wait<0>();
     }
-    __syncwarp();
+    if (gr.rank == 0) {
+      gflag[gr.id] = 0;
+      gbad[gr.id] = 0;
+    }
+    gsync<WG>(gr);
     if constexpr (EQ == 2 && !E::STAGE) {
       s.p[1] = const_cast<double*>(in0) + off;
       s.p[2] = const_cast<double*>(in1) + off;
     }
     int flag = 0;
-    run_variant<EQ, N, B>(VAR{}, s, &flag);
-    const bool fin = store_x<EQ, typename E::M0, N>(X + off, s.p[0]);
+    run_variant<EQ, N, B, WG>(VAR{}, s, &flag, gr);
+    const bool fin = store_x<EQ, typename E::M0, N, G>(X + off, s.p[0], gr.rank);
     const bool allfin = __all_sync(0xffffffffu, fin);
-    flag = __shfl_sync(0xffffffffu, flag, 0);
-    if (info && lane == 0) info[prob] = flag ? flag : (allfin ? 0 : -1);
-    __syncwarp();
+    if (gr.wig == 0 && lane == 0 && flag) gflag[gr.id] = flag;
+    if (lane == 0 && !allfin) atomicOr(&gbad[gr.id], 1);
+    gsync<WG>(gr);
+    if (info && gr.rank == 0) {
+      const int f = gflag[gr.id];
+      info[prob] = f ? f : (gbad[gr.id] ? -1 : 0);
+    }
     if constexpr (P::DB == 1) {
-      if (nxt < batch) issue_loads<EQ, N>(slot_at(0), in0, in1, in2, nxt * NN);
+      gsync<WG>(gr);  // slot reads done before it is refilled
+      if (nxt < batch) issue_loads<EQ, N, G>(slot_at(0), in0, in1, in2, nxt * NN, gr.rank);
     } else {
       cur ^= 1;
     }

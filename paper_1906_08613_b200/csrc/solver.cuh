@@ -267,12 +267,17 @@ __device__ __forceinline__ void sylv_tile4(const View& Lv, const View& Uv, const
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) w[a][b] = W.at(i0 + a, j0 + b);
-  double li[4], uj[4];
+  double li[4], uj[4], rp[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     li[a] = Lv.d(i0 + a);
     uj[a] = Uv.d(j0 + a);
   }
+  // reciprocal shifted pivots, off the substitution chain (<= 1 ulp)
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) rp[a][b] = 1.0 / (li[a] + uj[b]);
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
 #pragma unroll
@@ -287,7 +292,7 @@ __device__ __forceinline__ void sylv_tile4(const View& Lv, const View& Uv, const
       double acc = 0.0;
 #pragma unroll
       for (int c = 0; c < a; ++c) acc = fma(Lv.at(i0 + a, i0 + c), w[c][b], acc);
-      w[a][b] = (w[a][b] - acc) / (li[a] + uj[b]);
+      w[a][b] = (w[a][b] - acc) * rp[a][b];
     }
   }
 #pragma unroll
@@ -349,13 +354,14 @@ __device__ __forceinline__ void lyap_solve(const View& Lv, const View& W, int m,
     const int ihi = d >> 1;
     for (int i = ilo + g.rank; i <= ihi; i += G) {
       const int j = d - i;
+      const double rp = 1.0 / (Lv.d(i) + Lv.d(j));  // off the dot-product chain
       double acc = W.at(i, j);
       double d1 = 0.0, d2 = 0.0;
       for (int l = 0; l < i; ++l) d1 = fma(Lv.at(i, l), W.at(l, j), d1);
       for (int l = 0; l < j; ++l) d2 = fma(W.sym(i, l), Lv.at(j, l), d2);
       acc -= d1;
       acc -= d2;
-      W.ref(i, j) = acc / (Lv.d(i) + Lv.d(j));
+      W.ref(i, j) = acc * rp;
     }
     g.sync();
   }
