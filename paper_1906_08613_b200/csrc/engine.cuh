@@ -132,9 +132,11 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // A problem is owned by a group of WG warps (G = 32 * WG threads).
 struct Grp {
-  int rank;  // 0 .. G-1
-  int wig;   // warp in group
-  int id;    // group index in the CTA (named barrier id - 1)
+  int rank;     // 0 .. G-1
+  int wig;      // warp in group
+  int id;       // group index in the CTA (named barrier id - 1)
+  double* rsb;  // per-group reciprocal pivots of the last CHOL leaf (16)
+  double* scr;  // per-group split-K scratch ((WG - 1) * 256 doubles)
 };
 template <int WG>
 __device__ __forceinline__ void gsync(const Grp& g) {
@@ -150,8 +152,8 @@ struct AStream {
   KW<typename AV::Mat, AV::tr> w;
   KW<typename AV::Mat, !AV::tr> wm;  // mirror walker (SY only)
   int i_abs, k_abs;
-  __device__ __forceinline__ void init(const AV& v, int i) {
-    const int t = lane_id() & 3;
+  __device__ __forceinline__ void init(const AV& v, int i, int kofs = 0) {
+    const int t = (lane_id() & 3) + kofs;
     if constexpr (AV::sy) {
       i_abs = v.r0 + i;
       k_abs = v.c0 + t;
@@ -181,8 +183,8 @@ struct BStream {
   KW<typename BV::Mat, !BV::tr> w;
   KW<typename BV::Mat, BV::tr> wm;
   int j_abs, k_abs;
-  __device__ __forceinline__ void init(const BV& v, int j) {
-    const int t = lane_id() & 3;
+  __device__ __forceinline__ void init(const BV& v, int j, int kofs = 0) {
+    const int t = (lane_id() & 3) + kofs;
     if constexpr (BV::sy) {
       j_abs = v.c0 + j;
       k_abs = v.r0 + t;
@@ -220,7 +222,11 @@ __device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int
   const int g = lane >> 2, t = lane & 3;
   const int nbj = (q + 15) >> 4;
   const int nblk = ((m + 15) >> 4) * nbj;
-  for (int bk = gr.wig; bk < nblk; bk += WG) {
+  // a single output block and idle warps: split the k loop over the group
+  // and reduce the partial accumulators through shared memory (fixed order)
+  const bool splitk = (WG > 1) && (nblk == 1) && (p >= 16 * WG) && (gr.scr != nullptr);
+  const int nks = p >> 2;
+  for (int bk = splitk ? 0 : gr.wig; bk < nblk; bk += splitk ? 1 : WG) {
     {
       const int i0 = (bk / nbj) << 4, j0 = (bk % nbj) << 4;
       if (UP && i0 >= j0 + 16) continue;
@@ -233,14 +239,16 @@ __device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int
       const int ra1 = vi1 ? i0 + 8 + ((i0 + 8 + g < m) ? g : (g & 3)) : ra0;
       const int cb0 = j0 + ((j0 + g < q) ? g : (g & 3));
       const int cb1 = vj1 ? j0 + 8 + ((j0 + 8 + g < q) ? g : (g & 3)) : cb0;
+      const int ks0 = splitk ? (nks * gr.wig) / WG : 0;
+      const int ks1 = splitk ? (nks * (gr.wig + 1)) / WG : nks;
       AStream<AV> a0s, a1s;
       BStream<BV> b0s, b1s;
-      a0s.init(A, ra0);
-      a1s.init(A, ra1);
-      b0s.init(Bm, cb0);
-      b1s.init(Bm, cb1);
+      a0s.init(A, ra0, 4 * ks0);
+      a1s.init(A, ra1, 4 * ks0);
+      b0s.init(Bm, cb0, 4 * ks0);
+      b1s.init(Bm, cb1, 4 * ks0);
       double c00a = 0, c00b = 0, c01a = 0, c01b = 0, c10a = 0, c10b = 0, c11a = 0, c11b = 0;
-      for (int k0 = 0; k0 < p; k0 += 4) {
+      for (int ks = ks0; ks < ks1; ++ks) {
         const double a0 = a0s.load(A.base);
         const double b0 = b0s.load(Bm.base);
         const double a1 = a1s.load(A.base);
@@ -253,6 +261,21 @@ __device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int
         a1s.step();
         b0s.step();
         b1s.step();
+      }
+      if (splitk) {
+        double* sp = gr.scr + (gr.wig - 1) * 256 + lane * 8;
+        if (gr.wig > 0) {
+          sp[0] = c00a; sp[1] = c00b; sp[2] = c01a; sp[3] = c01b;
+          sp[4] = c10a; sp[5] = c10b; sp[6] = c11a; sp[7] = c11b;
+        }
+        gsync<WG>(gr);
+        if (gr.wig != 0) continue;
+#pragma unroll
+        for (int w = 1; w < WG; ++w) {
+          const double* q8 = gr.scr + (w - 1) * 256 + lane * 8;
+          c00a += q8[0]; c00b += q8[1]; c01a += q8[2]; c01b += q8[3];
+          c10a += q8[4]; c10b += q8[5]; c11a += q8[6]; c11b += q8[7];
+        }
       }
       auto wb = [&](int ib, int jb, double x0, double x1) {
         const int i = ib + g, j = jb + 2 * t;
@@ -294,7 +317,7 @@ __device__ __forceinline__ void trsm_b(const TVt& Tm, const WV& W, int q, const 
   if (gr.rank >= q) return;
   double rd[B];
 #pragma unroll
-  for (int i = 0; i < B; ++i) rd[i] = 1.0 / Tm.at(i, i);
+  for (int i = 0; i < B; ++i) rd[i] = (B <= 8) ? gr.rsb[i] : 1.0 / Tm.at(i, i);
   for (int j = gr.rank; j < q; j += 32 * WG) {
     double w[B];
 #pragma unroll
@@ -339,6 +362,45 @@ __device__ __forceinline__ void chol_leaf(const XV& W, int base, int* flag) {
 #pragma unroll
     for (int r = 0; r < B; ++r)
       if (r <= lane) W.ref(r, lane) = col[r];
+  }
+}
+
+// B <= 8: every lane of the warp factors the B x B block redundantly in
+// registers (no shuffles on the pivot chain); lane j < B writes column j back
+// and the reciprocal pivots 1/x_ii = rsqrt(a_ii) go to rsb for the TRSM.
+template <int B, class XV>
+__device__ __forceinline__ void chol_leaf_reg(const XV& W, int base, int* flag, double* rsb) {
+  const int lane = lane_id();
+  double t[B][B];
+#pragma unroll
+  for (int c = 0; c < B; ++c)
+#pragma unroll
+    for (int r = 0; r <= c; ++r) t[r][c] = W.at(r, c);
+  double rs[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    const double piv = t[i][i];
+    if (lane == 0 && piv <= 0.0 && *flag == 0) *flag = base + i + 1;
+    rs[i] = rsqrt(piv);
+    t[i][i] = piv * rs[i];
+#pragma unroll
+    for (int c = i + 1; c < B; ++c) t[i][c] *= rs[i];
+#pragma unroll
+    for (int r = i + 1; r < B; ++r)
+#pragma unroll
+      for (int c = r; c < B; ++c) t[r][c] = fma(-t[i][r], t[i][c], t[r][c]);
+  }
+#pragma unroll
+  for (int c = 0; c < B; ++c) {
+    if (lane == c) {
+#pragma unroll
+      for (int r = 0; r <= c; ++r) W.ref(r, c) = t[r][c];
+    }
+  }
+  if (lane < B) {
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+      if (lane == i) rsb[i] = rs[i];
   }
 }
 
@@ -568,7 +630,10 @@ __device__ __forceinline__ void exec(const Slot& s, const Rep<N, B>& rp, int* fl
     const auto Bw = mkv<E, Bv, SB>(s, rp.st(Bv::r), rp.st(Bv::c));
     gemm<UP, WG>(Ov, Av, Bw, m, p, q, S::sign < 0 ? -1.0 : 1.0, gr);
   } else if constexpr (S::kind == K_CHOL) {
-    if (gr.wig == 0) chol_leaf<B>(Ov, rp.st(O::r), flag);
+    if (gr.wig == 0) {
+      if constexpr (B <= 8) chol_leaf_reg<B>(Ov, rp.st(O::r), flag, gr.rsb);
+      else chol_leaf<B>(Ov, rp.st(O::r), flag);
+    }
   } else if constexpr (S::kind == K_TRSM) {
     using A = typename S::in0;
     const auto Tv = mkv<E, A, false>(s, rp.st(A::r), rp.st(A::c));
@@ -701,7 +766,11 @@ struct WPolicy {
   // warps per problem: smallest power of two reaching TARGET_WARPS per CTA
   static constexpr int WG = P >= TARGET_WARPS ? 1 : (2 * P >= TARGET_WARPS ? 2 : (4 * P >= TARGET_WARPS ? 4 : (8 * P >= TARGET_WARPS ? 8 : 16)));
   static constexpr int WARPS = P * WG;
-  static constexpr size_t SMEM = (size_t)P * DB * SLOT * 8 + 2 * 16 * sizeof(int);
+  static constexpr size_t BASE = (size_t)P * DB * SLOT * 8 + 2 * 16 * sizeof(int) + (size_t)16 * 16 * 8;
+  // split-K scratch per group (doubles), only where it still fits
+  static constexpr int SCR = (BASE + (size_t)P * (WG - 1) * 256 * 8 <= 227 * 1024) ? (WG - 1) * 256 : 0;
+  static constexpr size_t SMEM = (size_t)P * DB * SLOT * 8 + 2 * 16 * sizeof(int) + (size_t)16 * 16 * 8 +
+                                 (size_t)P * SCR * 8;
 };
 
 template <int EQ, int N, int G>
@@ -735,12 +804,16 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
   extern __shared__ double smem[];
   int* gflag = reinterpret_cast<int*>(smem + (size_t)P::P * P::DB * P::SLOT);
   int* gbad = gflag + 16;
+  double* rsb_all = reinterpret_cast<double*>(gbad + 16);
+  double* scr_all = rsb_all + 16 * 16;
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
   Grp gr;
   gr.id = warp / WG;
   gr.wig = warp % WG;
   gr.rank = threadIdx.x % G;
+  gr.rsb = rsb_all + 16 * gr.id;
+  gr.scr = P::SCR ? scr_all + (size_t)P::SCR * gr.id : nullptr;
   auto slot_at = [&](int d) {
     Slot sl;
     double* base = smem + ((size_t)gr.id * P::DB + (d % P::DB)) * P::SLOT;
