@@ -71,19 +71,20 @@ def batch_for(n):
     return (1 << 28) // (8 * n * n)
 
 
-def workload(name, world):
-    """(eq, [(n, batch_per_rank, seed)], scaling, description)."""
+def workload(name, world, rank=0):
+    """(eq, [(n, batch_this_rank, seed, first_index)], scaling, description)."""
+    from paper_1906_08613_b200.shard import shard_range, weak_range
     if name.endswith("-sweep"):
         eq = EQS[name.split("-")[0]]
-        return eq, [(n, batch_for(n), n) for n in SIZES], "weak", \
+        return eq, [(n, batch_for(n), n, weak_range(batch_for(n), rank)[0]) for n in SIZES], "weak", \
             f"{eq} sweep n=4..128 step 4, batch floor(2^28/8n^2) per GPU, seed n"
     if name == "c1":
-        return "cholesky", [(16, 4096, 0)], "weak", "cholesky n=16 batch 4096 seed 0 (L2 flushed between steps)"
+        return "cholesky", [(16, 4096, 0, weak_range(4096, rank)[0])], "weak", \
+            "cholesky n=16 batch 4096 seed 0 (L2 flushed between steps)"
     if name.startswith("c5-"):
         eq = EQS[name.split("-")[1]]
-        total = 1 << 20
-        per = -(-total // world)
-        return eq, [(64, per, 7)], "strong", f"{eq} n=64, 2^20 problems sharded over GPUs, seed 7"
+        first, count = shard_range(1 << 20, rank, world)
+        return eq, [(64, count, 7, first)], "strong", f"{eq} n=64, 2^20 problems sharded over GPUs, seed 7"
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -186,8 +187,8 @@ def run_sweep(eq, cases, rank, steps, warmup, peaks, flush_l2=False, per_n_reps=
     stream = torch.cuda.Stream()
     plans = []
     with torch.cuda.stream(stream):
-        for n, batch, seed in cases:
-            ins = executor.generate(eq, n, seed, batch, first=rank * batch, stream=stream)
+        for n, batch, seed, first in cases:
+            ins = executor.generate(eq, n, seed, batch, first=first, stream=stream)
             plans.append(executor.Plan(eq, ins))
     stream.synchronize()
     # first launches (sets kernel attributes outside capture) + check
@@ -326,14 +327,14 @@ def cpu_baseline(eq, cases, budget_s=12.0, inputs_from=None, seed_first=0):
     ref = build_ref.RefLib() if use_ref else None
     per_size_budget = budget_s / len(cases)
     tot_flops, tot_time, detail = 0.0, 0.0, []
-    for ci, (n, batch, seed) in enumerate(cases):
+    for ci, (n, batch, seed, first) in enumerate(cases):
         # sample size: aim at ~per_size_budget/2 for the timed run
         est_ns = {"cholesky": 0.35, "lyapunov": 0.8, "sylvester": 1.1}[eq] * n ** 3 / cores
         s = int(max(cores, min(batch, per_size_budget * 0.5 / (est_ns * 1e-9))))
         if inputs_from is not None:
             ins = [t[:s].cpu().numpy() for t in inputs_from[ci]]
         else:
-            ins = oracle.generate(eq, n, seed, seed_first, s)
+            ins = oracle.generate(eq, n, seed, first, s)
         if ref is not None:
             cands = ref.kernels(eq, n)
             best = None
@@ -432,7 +433,7 @@ def main():
 
     world, rank, local = dist_setup(args.gpus)
     peaks = measured_peaks()
-    eq, cases, scaling, desc = workload(args.workload, world)
+    eq, cases, scaling, desc = workload(args.workload, world, rank)
     clocks = ClockSampler(local)
     barrier(world)
     res = run_sweep(eq, cases, rank, args.steps, warmup, peaks, flush_l2=(args.workload == "c1"),
@@ -473,7 +474,7 @@ def main():
     if args.workload == "chol-sweep" and not args.no_extra:
         extra = {}
         for wl in ("lyap-sweep", "sylv-sweep"):
-            eq2, cases2, _, desc2 = workload(wl, world)
+            eq2, cases2, _, desc2 = workload(wl, world, rank)
             r2 = run_sweep(eq2, cases2, rank, args.steps, warmup, peaks)
             v2, ms2, roof2 = summarize(eq2, r2, args.steps, peaks, world)
             extra[eq2] = {"value": round(v2, 2), "unit": "GFLOP/s", "ms_per_step": round(ms2, 4),
@@ -501,7 +502,7 @@ def reference_arm(args, warmup):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    eq, cases, scaling, desc = workload(args.workload, 1)
+    eq, cases, scaling, desc = workload(args.workload, 1, 0)
     # each step: a bounded sample of every size, throughput extrapolated
     budget = max(1.0, 60.0 / (args.steps + warmup))
     for _ in range(warmup):

@@ -281,10 +281,12 @@ int lagen_b200_sylvester(int variant, int n, int b, long long batch, const doubl
   return run_variant(LAGEN_SYLVESTER, variant, n, b, batch, in, X, info, stream);
 }
 
-// Host-buffer pipeline: chunks of the batch cycle through two device
-// buffer sets on two streams so H2D(c+1), solve(c) and D2H(c-1) overlap.
+// Host-buffer pipeline: chunks of the batch cycle through NS device buffer
+// sets on NS streams so the H2D engine, the SMs and the D2H engine all stay
+// busy (with 2 sets the H2D of chunk c+2 would wait for the D2H of chunk c).
 int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                             const double* const* h_inputs, double* h_X, int* h_info) {
+  constexpr int NS = 4;
   int rc = check_common(eq, n, b, batch);
   if (rc) return rc;
   rc = validate(eq, stmts, nstmts);
@@ -295,16 +297,18 @@ int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, 
   for (int i = 0; i < nin; ++i)
     if (!h_inputs[i]) return fail(LAGEN_EINVAL, "null input buffer");
   const size_t prob_bytes = sizeof(double) * (size_t)n * n;
-  // ~32 MiB of input per chunk and operand, at least one problem
-  long long chunk = (32ll << 20) / (long long)prob_bytes;
+  // ~16 MiB of input per chunk and operand, at least one problem
+  long long chunk = (16ll << 20) / (long long)prob_bytes;
   if (chunk < 1) chunk = 1;
   if (chunk > batch) chunk = batch;
-  cudaStream_t st[2] = {nullptr, nullptr};
-  double* d_in[2][3] = {{nullptr}};
-  double* d_X[2] = {nullptr, nullptr};
-  int* d_info[2] = {nullptr, nullptr};
+  cudaStream_t st[NS] = {nullptr};
+  double* d_in[NS][3] = {{nullptr}};
+  double* d_X[NS] = {nullptr};
+  int* d_info[NS] = {nullptr};
   cudaError_t err = cudaSuccess;
-  for (int k = 0; k < 2 && err == cudaSuccess; ++k) {
+  const long long nchunks = (batch + chunk - 1) / chunk;
+  const int ns = nchunks < NS ? (int)nchunks : NS;
+  for (int k = 0; k < ns && err == cudaSuccess; ++k) {
     err = cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
     for (int i = 0; i < nin && err == cudaSuccess; ++i) err = cudaMallocAsync(&d_in[k][i], chunk * prob_bytes, st[k]);
     if (err == cudaSuccess) err = cudaMallocAsync(&d_X[k], chunk * prob_bytes, st[k]);
@@ -313,7 +317,7 @@ int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, 
   int status = LAGEN_OK;
   if (err != cudaSuccess) status = cuda_fail(err, "host pipeline setup");
   for (long long c0 = 0, it = 0; status == LAGEN_OK && c0 < batch; c0 += chunk, ++it) {
-    const int k = (int)(it & 1);
+    const int k = (int)(it % ns);
     const long long cnt = (batch - c0) < chunk ? (batch - c0) : chunk;
     for (int i = 0; i < nin && err == cudaSuccess; ++i)
       err = cudaMemcpyAsync(d_in[k][i], h_inputs[i] + c0 * n * n, cnt * prob_bytes, cudaMemcpyHostToDevice, st[k]);
@@ -326,7 +330,7 @@ int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, 
       err = cudaMemcpyAsync(h_info + c0, d_info[k], cnt * sizeof(int), cudaMemcpyDeviceToHost, st[k]);
     if (err != cudaSuccess) { status = cuda_fail(err, "D2H"); break; }
   }
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < ns; ++k) {
     if (!st[k]) continue;
     for (int i = 0; i < 3; ++i)
       if (d_in[k][i]) cudaFreeAsync(d_in[k][i], st[k]);
