@@ -120,6 +120,12 @@ int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b
 int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
                               long long batch, const double* const* inputs, double* X,
                               int* info, void* stream, int engine);
+/* Same as lagen_b200_execute_engine; for warp-engine launches, d_prof (device,
+ * >= 32 zeroed uint64) receives cycle counts per phase / schedule level of
+ * one problem group (tools/phase_profile.py).  Profiling aid only. */
+int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
+                               long long batch, const double* const* inputs, double* X,
+                               int* info, void* stream, int engine, unsigned long long* d_prof);
 /* 1 if the warp engine has an instance for (eq, n, b, built-in variant) */
 int lagen_b200_warp_supported(int eq, int n, int b, int variant);
 /* 1 if `engine` has an instance for (eq, n, b, built-in variant) */

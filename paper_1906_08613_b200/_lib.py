@@ -41,6 +41,7 @@ def _load():
     lib.lagen_b200_execute.argtypes = [i, vp, i, i, i, ll, vp, vp, vp, vp]
     lib.lagen_b200_execute_engine.argtypes = [i, vp, i, i, i, ll, vp, vp, vp, vp, i]
     lib.lagen_b200_warp_supported.argtypes = [i, i, i, i]
+    lib.lagen_b200_execute_profile.argtypes = [i, vp, i, i, i, ll, vp, vp, vp, vp, i, vp]
     lib.lagen_b200_engine_supported.argtypes = [i, i, i, i, i]
     lib.lagen_b200_execute_host.argtypes = [i, vp, i, i, i, ll, vp, vp, vp]
     lib.lagen_b200_generate.argtypes = [i, i, ctypes.c_ulonglong, ll, ll, vp, vp]
@@ -59,6 +60,7 @@ EXPORTED = (
     "lagen_b200_cholesky", "lagen_b200_lyapunov", "lagen_b200_sylvester",
     "lagen_b200_execute", "lagen_b200_execute_host", "lagen_b200_generate",
     "lagen_b200_execute_engine", "lagen_b200_warp_supported", "lagen_b200_engine_supported",
+    "lagen_b200_execute_profile",
 )
 ENGINES = {"auto": 0, "generic": 1, "warp": 2, "column": 3}
 

@@ -25,6 +25,7 @@
 #include <stdint.h>
 
 #include <type_traits>
+#include <utility>
 
 #include "lagen_b200.h"
 
@@ -36,6 +37,11 @@ enum { K_GEMM = 0, K_CHOL = 1, K_TRSM = 2, K_SYLV = 3, K_LYAP = 4 };
 
 __device__ __forceinline__ int swz(int r, int c, int key) {
   return (((((r & 3) << 1) | ((c & 3) >> 1)) ^ key) << 1) | (c & 1);
+}
+
+// offset inside a tile whose base (tile_index * 16) and key ((R ^ C) & 7) are known
+__device__ __forceinline__ int tile_off(int tbase, int key, int r, int c) {
+  return tbase + ((((((r & 3) << 1) | ((c & 3) >> 1)) ^ key) & 7) << 1) + (c & 1);
 }
 
 template <int T, int LY>
@@ -135,9 +141,19 @@ struct Grp {
   int rank;     // 0 .. G-1
   int wig;      // warp in group
   int id;       // group index in the CTA (named barrier id - 1)
-  double* rsb;  // per-group reciprocal pivots of the last CHOL leaf (16)
+  double* rsb;  // per-group: reciprocal pivots of the last CHOL leaf [0, 16) and
+                //            its factor, row-major B x B, at [16, 16 + B*B)
   double* scr;  // per-group split-K scratch ((WG - 1) * 256 doubles)
+  unsigned long long* prof;  // cycle accounting buffer (profiling launches only)
 };
+// The warps / threads executing one statement: the whole group, or (when a
+// CHOL leaf occupies warp 0 in the same dependency level) warps 1 .. WG-1.
+struct Sub {
+  int w, nw;        // warp index within the subset, subset size (warps)
+  int rank, nthr;   // thread index within the subset, subset size (threads)
+  bool full;        // whole group (group barriers allowed)
+};
+
 template <int WG>
 __device__ __forceinline__ void gsync(const Grp& g) {
   if constexpr (WG == 1) __syncwarp();
@@ -215,18 +231,100 @@ struct BStream {
 // 8-row/col tiles read clamped (valid) rows and discard them on write.
 // UP: upper target (only i <= j written; tiles strictly below skipped).
 // ----------------------------------------------------------------------------
+// m <= 8 (block-row updates of the left-looking variants): 8 x 32 warp
+// blocks, one A fragment feeds four independent DMMA accumulators per k-step.
+template <bool UP, class OV, class AV, class BV>
+__device__ __forceinline__ void gemm_row8(const OV& O, const AV& A, const BV& Bm, int m, int p, int q, double sgn,
+                                          const Sub& sb) {
+  const int lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int nblk = (q + 31) >> 5;
+  const int ra = (g < m) ? g : (g & 3);
+  for (int bk = sb.w; bk < nblk; bk += sb.nw) {
+    const int j0 = bk << 5;
+    bool v[4];
+    int cb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int jt = j0 + 8 * u;
+      v[u] = jt < q && !(UP && 0 >= jt + 8);
+      cb[u] = (jt + g < q) ? jt + g : (jt < q ? jt + (g & 3) : j0 + (g & 3));
+    }
+    AStream<AV> as;
+    BStream<BV> bs[4];
+    as.init(A, ra, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bs[u].init(Bm, cb[u], 0);
+    // two accumulator sets (even / odd k-steps): eight independent DMMA
+    // chains per warp hide the DMMA latency
+    double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
+    double e0[4] = {0, 0, 0, 0}, e1[4] = {0, 0, 0, 0};
+    int k0 = 0;
+    for (; k0 + 8 <= p; k0 += 8) {
+      const double a = as.load(A.base);
+      double bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bv[u] = v[u] ? bs[u].load(Bm.base) : 0.0;
+      as.step();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bs[u].step();
+      const double a2 = as.load(A.base);
+      double bw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bw[u] = v[u] ? bs[u].load(Bm.base) : 0.0;
+      as.step();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bs[u].step();
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (v[u]) dmma(c0[u], c1[u], a, bv[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (v[u]) dmma(e0[u], e1[u], a2, bw[u]);
+    }
+    if (k0 < p) {
+      const double a = as.load(A.base);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (v[u]) dmma(c0[u], c1[u], a, bs[u].load(Bm.base));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      c0[u] += e0[u];
+      c1[u] += e1[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (!v[u]) continue;
+      const int i = g, j = j0 + 8 * u + 2 * t;
+      if (i < m && j < q && (!UP || i <= j)) {
+        double& o0 = O.ref(i, j);
+        o0 = fma(sgn, c0[u], o0);
+      }
+      if (i < m && j + 1 < q && (!UP || i <= j + 1)) {
+        double& o1 = O.ref(i, j + 1);
+        o1 = fma(sgn, c1[u], o1);
+      }
+    }
+  }
+}
+
 template <bool UP, int WG, class OV, class AV, class BV>
 __device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int m, int p, int q, double sgn,
-                                     const Grp& gr) {
+                                     const Grp& gr, const Sub& sb) {
+  if (m <= 8 && q > 8) {
+    gemm_row8<UP>(O, A, Bm, m, p, q, sgn, sb);
+    return;
+  }
   const int lane = lane_id();
   const int g = lane >> 2, t = lane & 3;
   const int nbj = (q + 15) >> 4;
   const int nblk = ((m + 15) >> 4) * nbj;
   // a single output block and idle warps: split the k loop over the group
   // and reduce the partial accumulators through shared memory (fixed order)
-  const bool splitk = (WG > 1) && (nblk == 1) && (p >= 16 * WG) && (gr.scr != nullptr);
+  const bool splitk = (WG > 1) && sb.full && (nblk == 1) && (p >= 16 * WG) && (gr.scr != nullptr);
   const int nks = p >> 2;
-  for (int bk = splitk ? 0 : gr.wig; bk < nblk; bk += splitk ? 1 : WG) {
+  for (int bk = splitk ? 0 : sb.w; bk < nblk; bk += splitk ? 1 : sb.nw) {
     {
       const int i0 = (bk / nbj) << 4, j0 = (bk % nbj) << 4;
       if (UP && i0 >= j0 + 16) continue;
@@ -301,8 +399,8 @@ __device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int
 // ----------------------------------------------------------------------------
 // general m (Cholesky v0: coefficient X_00^T, m = kb): lanes own columns.
 template <int WG, class TVt, class WV>
-__device__ __forceinline__ void trsm(const TVt& Tm, const WV& W, int m, int q, const Grp& gr) {
-  for (int j = gr.rank; j < q; j += 32 * WG) {
+__device__ __forceinline__ void trsm(const TVt& Tm, const WV& W, int m, int q, const Grp& gr, const Sub& sb) {
+  for (int j = sb.rank; j < q; j += sb.nthr) {
     for (int i = 0; i < m; ++i) {
       double s = W.at(i, j);
       for (int l = 0; l < i; ++l) s = fma(-Tm.at(i, l), W.at(l, j), s);
@@ -313,24 +411,53 @@ __device__ __forceinline__ void trsm(const TVt& Tm, const WV& W, int m, int q, c
 
 // compile-time m = B <= 16: column in registers, reciprocal pivots.
 template <int B, int WG, class TVt, class WV>
-__device__ __forceinline__ void trsm_b(const TVt& Tm, const WV& W, int q, const Grp& gr) {
-  if (gr.rank >= q) return;
-  double rd[B];
+__device__ __forceinline__ void trsm_b(const TVt& Tm, const WV& W, int q, const Grp& gr, const Sub& sb) {
+  if (sb.rank >= q) return;
+  using M = typename WV::Mat;
+  if constexpr (B <= 8 && !WV::tr && !WV::sy) {
+    // coefficient = factor of this iteration's CHOL leaf (rsb: reciprocal
+    // pivots, then the factor row-major): T(i, l) = X(l, i) = fac[l][i]
+    const double* fac = gr.rsb + 16;
+    const int R0 = W.r0 >> 2;
+    for (int j = sb.rank; j < q; j += sb.nthr) {
+      const int c = W.c0 + j, C = c >> 2;
+      int tb[B / 4], ky[B / 4];
 #pragma unroll
-  for (int i = 0; i < B; ++i) rd[i] = (B <= 8) ? gr.rsb[i] : 1.0 / Tm.at(i, i);
-  for (int j = gr.rank; j < q; j += 32 * WG) {
-    double w[B];
+      for (int i = 0; i < B / 4; ++i) {
+        tb[i] = M::tidx(R0 + i, C) << 4;
+        ky[i] = ((R0 + i) ^ C) & 7;
+      }
+      double w[B];
 #pragma unroll
-    for (int i = 0; i < B; ++i) w[i] = W.at(i, j);
+      for (int i = 0; i < B; ++i) w[i] = W.base[tile_off(tb[i / 4], ky[i / 4], i, c)];
 #pragma unroll
-    for (int i = 0; i < B; ++i) {
-      double s = w[i];
+      for (int i = 0; i < B; ++i) {
+        double v = w[i];
 #pragma unroll
-      for (int l = 0; l < i; ++l) s = fma(-Tm.at(i, l), w[l], s);
-      w[i] = s * rd[i];
+        for (int l = 0; l < i; ++l) v = fma(-fac[l * B + i], w[l], v);
+        w[i] = v * gr.rsb[i];
+      }
+#pragma unroll
+      for (int i = 0; i < B; ++i) W.base[tile_off(tb[i / 4], ky[i / 4], i, c)] = w[i];
     }
+  } else {
+    double rd[B];
 #pragma unroll
-    for (int i = 0; i < B; ++i) W.ref(i, j) = w[i];
+    for (int i = 0; i < B; ++i) rd[i] = 1.0 / Tm.at(i, i);
+    for (int j = sb.rank; j < q; j += sb.nthr) {
+      double w[B];
+#pragma unroll
+      for (int i = 0; i < B; ++i) w[i] = W.at(i, j);
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        double v = w[i];
+#pragma unroll
+        for (int l = 0; l < i; ++l) v = fma(-Tm.at(i, l), w[l], v);
+        w[i] = v * rd[i];
+      }
+#pragma unroll
+      for (int i = 0; i < B; ++i) W.ref(i, j) = w[i];
+    }
   }
 }
 
@@ -370,17 +497,42 @@ __device__ __forceinline__ void chol_leaf(const XV& W, int base, int* flag) {
 // and the reciprocal pivots 1/x_ii = rsqrt(a_ii) go to rsb for the TRSM.
 template <int B, class XV>
 __device__ __forceinline__ void chol_leaf_reg(const XV& W, int base, int* flag, double* rsb) {
+  using M = typename XV::Mat;
+  constexpr int TB = B / 4;
   const int lane = lane_id();
+  // tile bases / keys of the diagonal block (r0 == c0, multiple of 4)
+  const int K = W.r0 >> 2;
+  int tb[TB][TB], ky[TB][TB];
+#pragma unroll
+  for (int i = 0; i < TB; ++i)
+#pragma unroll
+    for (int j = i; j < TB; ++j) {
+      tb[i][j] = M::tidx(K + i, K + j) << 4;
+      ky[i][j] = ((K + i) ^ (K + j)) & 7;
+    }
+  // whole tiles as 16-byte chunks (uniform addresses -> broadcast loads)
   double t[B][B];
 #pragma unroll
-  for (int c = 0; c < B; ++c)
+  for (int i = 0; i < TB; ++i)
 #pragma unroll
-    for (int r = 0; r <= c; ++r) t[r][c] = W.at(r, c);
+    for (int j = i; j < TB; ++j)
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        const double2 v = *reinterpret_cast<const double2*>(W.base + tb[i][j] + (((ch ^ ky[i][j]) & 7) << 1));
+        const int r = 4 * i + (ch >> 1), c = 4 * j + 2 * (ch & 1);
+        t[r][c] = v.x;
+        t[r][c + 1] = v.y;
+      }
   double rs[B];
+  bool bad = false;
+  int badi = 0;
 #pragma unroll
   for (int i = 0; i < B; ++i) {
     const double piv = t[i][i];
-    if (lane == 0 && piv <= 0.0 && *flag == 0) *flag = base + i + 1;
+    if (!bad && piv <= 0.0) {
+      bad = true;
+      badi = i;
+    }
     rs[i] = rsqrt(piv);
     t[i][i] = piv * rs[i];
 #pragma unroll
@@ -390,17 +542,19 @@ __device__ __forceinline__ void chol_leaf_reg(const XV& W, int base, int* flag, 
 #pragma unroll
       for (int c = r; c < B; ++c) t[r][c] = fma(-t[i][r], t[i][c], t[r][c]);
   }
+  if (lane == 0) {
+    if (bad && *flag == 0) *flag = base + badi + 1;
+    // factor back into the tiles (upper elements only), the row-major
+    // factor and the reciprocal pivots for this iteration's TRSM
 #pragma unroll
-  for (int c = 0; c < B; ++c) {
-    if (lane == c) {
+    for (int c = 0; c < B; ++c) {
 #pragma unroll
-      for (int r = 0; r <= c; ++r) W.ref(r, c) = t[r][c];
+      for (int r = 0; r <= c; ++r) {
+        W.base[tile_off(tb[r / 4][c / 4], ky[r / 4][c / 4], r, c)] = t[r][c];
+        rsb[16 + r * B + c] = t[r][c];
+      }
+      rsb[c] = rs[c];
     }
-  }
-  if (lane < B) {
-#pragma unroll
-    for (int i = 0; i < B; ++i)
-      if (lane == i) rsb[i] = rs[i];
   }
 }
 
@@ -612,7 +766,7 @@ __device__ __forceinline__ TV<typename MatOf<E, Vw::op>::type, Vw::tr != 0, SY> 
 }
 
 template <int EQ, int N, int B, int WG, class S>
-__device__ __forceinline__ void exec(const Slot& s, const Rep<N, B>& rp, int* flag, const Grp& gr) {
+__device__ __forceinline__ void exec(const Slot& s, const Rep<N, B>& rp, int* flag, const Grp& gr, const Sub& sb) {
   using E = EqT<EQ, N>;
   using O = typename S::out;
   const int m = rp.ex(O::r), q = rp.ex(O::c);
@@ -628,7 +782,7 @@ __device__ __forceinline__ void exec(const Slot& s, const Rep<N, B>& rp, int* fl
     constexpr bool SB = E::SYMX && Bv::op == 0 && Bv::r == Bv::c;
     const auto Av = mkv<E, A, SA>(s, rp.st(A::r), rp.st(A::c));
     const auto Bw = mkv<E, Bv, SB>(s, rp.st(Bv::r), rp.st(Bv::c));
-    gemm<UP, WG>(Ov, Av, Bw, m, p, q, S::sign < 0 ? -1.0 : 1.0, gr);
+    gemm<UP, WG>(Ov, Av, Bw, m, p, q, S::sign < 0 ? -1.0 : 1.0, gr, sb);
   } else if constexpr (S::kind == K_CHOL) {
     if (gr.wig == 0) {
       if constexpr (B <= 8) chol_leaf_reg<B>(Ov, rp.st(O::r), flag, gr.rsb);
@@ -637,8 +791,8 @@ __device__ __forceinline__ void exec(const Slot& s, const Rep<N, B>& rp, int* fl
   } else if constexpr (S::kind == K_TRSM) {
     using A = typename S::in0;
     const auto Tv = mkv<E, A, false>(s, rp.st(A::r), rp.st(A::c));
-    if constexpr (O::r == 1) trsm_b<B, WG>(Tv, Ov, q, gr);  // m == B
-    else trsm<WG>(Tv, Ov, m, q, gr);
+    if constexpr (O::r == 1) trsm_b<B, WG>(Tv, Ov, q, gr, sb);  // m == B
+    else trsm<WG>(Tv, Ov, m, q, gr, sb);
   } else if constexpr (S::kind == K_SYLV) {
     using A = typename S::in0;
     using Bv = typename S::in1;
@@ -651,15 +805,119 @@ __device__ __forceinline__ void exec(const Slot& s, const Rep<N, B>& rp, int* fl
     const auto Ws = mkv<E, O, true>(s, rp.st(O::r), rp.st(O::c));
     lyap<WG>(Lv, Ov, Ws, m, gr);
   }
+}
+
+// ----------------------------------------------------------------------------
+// Per-iteration schedule (compile time).  Statements are grouped into
+// dependency levels (as-late-as-possible, so an independent update floats
+// next to the statement that needs it last); statements of one level touch
+// disjoint blocks, so they run back to back without a barrier, and a CHOL
+// leaf (one warp) shares its level with the other statements running on the
+// remaining warps.  Results are bitwise those of program order.
+// ----------------------------------------------------------------------------
+struct SD {
+  int kind, oop, orr, oc;
+  int iop[2], ir[2], ic[2];
+};
+template <class S>
+constexpr SD make_sd() {
+  return SD{S::kind, S::out::op, S::out::r, S::out::c,
+            {S::in0::op, S::in1::op}, {S::in0::r, S::in1::r}, {S::in0::c, S::in1::c}};
+}
+constexpr bool sd_reads(const SD& a, int op, int r, int c) {
+  if (a.oop == op && a.orr == r && a.oc == c) return true;  // read-modify-write
+  for (int t = 0; t < 2; ++t)
+    if (a.iop[t] == op && a.ir[t] == r && a.ic[t] == c) return true;
+  return false;
+}
+constexpr bool sd_dep(const SD& a, const SD& b) {  // b (later) depends on a
+  return sd_reads(b, a.oop, a.orr, a.oc) || sd_reads(a, b.oop, b.orr, b.oc);
+}
+template <int M>
+struct Sched {
+  int level[M > 0 ? M : 1];
+  int nlevels;
+  int leaf_level_has_leaf[M > 0 ? M : 1];
+  constexpr Sched(const SD* d) : level{}, nlevels(0), leaf_level_has_leaf{} {
+    int asap[M > 0 ? M : 1] = {};
+    for (int j = 0; j < M; ++j) {
+      asap[j] = 0;
+      for (int i = 0; i < j; ++i)
+        if (sd_dep(d[i], d[j]) && asap[i] + 1 > asap[j]) asap[j] = asap[i] + 1;
+    }
+    int depth = 0;
+    for (int j = 0; j < M; ++j)
+      if (asap[j] + 1 > depth) depth = asap[j] + 1;
+    // as late as possible
+    for (int j = M - 1; j >= 0; --j) {
+      int l = depth - 1;
+      for (int k = j + 1; k < M; ++k)
+        if (sd_dep(d[j], d[k]) && level[k] - 1 < l) l = level[k] - 1;
+      level[j] = l;
+    }
+    nlevels = depth;
+    for (int j = 0; j < M; ++j) leaf_level_has_leaf[j] = 0;
+    for (int j = 0; j < M; ++j)
+      if (d[j].kind == K_CHOL) leaf_level_has_leaf[level[j]] = 1;
+  }
+};
+
+template <class... S>
+struct VarInfo {
+  static constexpr int M = sizeof...(S);
+  static constexpr SD d[M] = {make_sd<S>()...};
+  static constexpr Sched<M> sch{d};
+};
+
+template <int EQ, int N, int B, int WG, int L, class INFO, class S, int I>
+__device__ __forceinline__ void exec_if(const Slot& s, const Rep<N, B>& rp, int* flag, const Grp& gr) {
+  if constexpr (INFO::sch.level[I] == L) {
+    constexpr bool shared_level = (WG > 1) && INFO::sch.leaf_level_has_leaf[L] && S::kind != K_CHOL;
+    Sub sb;
+    if constexpr (shared_level) {
+      if (gr.wig == 0) return;  // warp 0 runs the leaf of this level
+      sb.w = gr.wig - 1;
+      sb.nw = WG - 1;
+      sb.rank = gr.rank - 32;
+      sb.nthr = 32 * (WG - 1);
+      sb.full = false;
+    } else {
+      sb.w = gr.wig;
+      sb.nw = WG;
+      sb.rank = gr.rank;
+      sb.nthr = 32 * WG;
+      sb.full = true;
+    }
+    exec<EQ, N, B, WG, S>(s, rp, flag, gr, sb);
+  }
+}
+
+// Optional cycle accounting (tools/phase_profile.py): when the launch passes
+// a profile buffer, thread 0 of group 0 in CTA 0 adds the cycles of each
+// schedule level ([4 + L]) and phase ([0] wait, [1] compute, [2] store,
+// [3] problems) to it.
+template <int EQ, int N, int B, int WG, int L, class INFO, class... S, size_t... I>
+__device__ __forceinline__ void run_level(const Slot& s, const Rep<N, B>& rp, int* flag, const Grp& gr,
+                                          std::index_sequence<I...>) {
+  const long long t0 = clock64();
+  (exec_if<EQ, N, B, WG, L, INFO, S, (int)I>(s, rp, flag, gr), ...);
   gsync<WG>(gr);
+  if (gr.prof) gr.prof[4 + L] += clock64() - t0;
+}
+
+template <int EQ, int N, int B, int WG, class INFO, class... S, int... Ls>
+__device__ __forceinline__ void run_iter(const Slot& s, const Rep<N, B>& rp, int* flag, const Grp& gr,
+                                         std::integer_sequence<int, Ls...>) {
+  (run_level<EQ, N, B, WG, Ls, INFO, S...>(s, rp, flag, gr, std::index_sequence_for<S...>{}), ...);
 }
 
 template <int EQ, int N, int B, int WG, class... S>
 __device__ __forceinline__ void run_variant(Var<S...>, const Slot& s, int* flag, const Grp& gr) {
+  using INFO = VarInfo<S...>;
 #pragma unroll 1
   for (int k = 0; k < N / B; ++k) {
     Rep<N, B> rp{k};
-    (exec<EQ, N, B, WG, S>(s, rp, flag, gr), ...);
+    run_iter<EQ, N, B, WG, INFO, S...>(s, rp, flag, gr, std::make_integer_sequence<int, INFO::sch.nlevels>{});
   }
 }
 
@@ -701,6 +959,7 @@ __device__ __forceinline__ bool store_x(double* __restrict__ dst, const double* 
   constexpr int T = N / 4;
   constexpr int UNITS = T * 4 * T;
   bool finite = true;
+#pragma unroll 4
   for (int u = rank; u < UNITS; u += G) {
     const int C = u % T;
     const int rr = (u / T) & 3;
@@ -757,8 +1016,8 @@ struct WPolicy {
   static constexpr int BUDGET = 220 * 1024;
   static constexpr int TARGET_WARPS = 12;
   // problem slots that fit single / double buffered
-  static constexpr int S1 = BUDGET / (SLOT * 8);
-  static constexpr int S2 = BUDGET / (2 * SLOT * 8);
+  static constexpr int S1 = BUDGET / (SLOT * 8 + 640);      // + per-group pivots / factor scratch
+  static constexpr int S2 = BUDGET / (2 * SLOT * 8 + 640);
   // double-buffer (prefetch the next problem) when >= 6 problems still fit
   static constexpr int DB = S2 >= 6 ? 2 : 1;
   static constexpr int P0 = DB == 2 ? S2 : (S1 < 1 ? 1 : S1);
@@ -766,11 +1025,11 @@ struct WPolicy {
   // warps per problem: smallest power of two reaching TARGET_WARPS per CTA
   static constexpr int WG = P >= TARGET_WARPS ? 1 : (2 * P >= TARGET_WARPS ? 2 : (4 * P >= TARGET_WARPS ? 4 : (8 * P >= TARGET_WARPS ? 8 : 16)));
   static constexpr int WARPS = P * WG;
-  static constexpr size_t BASE = (size_t)P * DB * SLOT * 8 + 2 * 16 * sizeof(int) + (size_t)16 * 16 * 8;
+  static constexpr int RSB = 16 + 64;  // reciprocal pivots + B<=8 factor, per group
+  static constexpr size_t BASE = (size_t)P * DB * SLOT * 8 + 2 * 16 * sizeof(int) + (size_t)P * RSB * 8;
   // split-K scratch per group (doubles), only where it still fits
   static constexpr int SCR = (BASE + (size_t)P * (WG - 1) * 256 * 8 <= 227 * 1024) ? (WG - 1) * 256 : 0;
-  static constexpr size_t SMEM = (size_t)P * DB * SLOT * 8 + 2 * 16 * sizeof(int) + (size_t)16 * 16 * 8 +
-                                 (size_t)P * SCR * 8;
+  static constexpr size_t SMEM = BASE + (size_t)P * SCR * 8;
 };
 
 template <int EQ, int N, int G>
@@ -797,7 +1056,8 @@ __device__ __forceinline__ void issue_loads(const Slot& s, const double* in0, co
 template <int EQ, int N, int B, class VAR>
 __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
     warp_kernel(const double* __restrict__ in0, const double* __restrict__ in1, const double* __restrict__ in2,
-                double* __restrict__ X, int* __restrict__ info, long long batch) {
+                double* __restrict__ X, int* __restrict__ info, long long batch,
+                unsigned long long* __restrict__ prof) {
   using E = EqT<EQ, N>;
   using P = WPolicy<EQ, N>;
   constexpr int WG = P::WG, G = WG * 32;
@@ -805,15 +1065,16 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
   int* gflag = reinterpret_cast<int*>(smem + (size_t)P::P * P::DB * P::SLOT);
   int* gbad = gflag + 16;
   double* rsb_all = reinterpret_cast<double*>(gbad + 16);
-  double* scr_all = rsb_all + 16 * 16;
+  double* scr_all = rsb_all + P::P * P::RSB;
   const int warp = threadIdx.x >> 5;
   const int lane = lane_id();
   Grp gr;
   gr.id = warp / WG;
   gr.wig = warp % WG;
   gr.rank = threadIdx.x % G;
-  gr.rsb = rsb_all + 16 * gr.id;
+  gr.rsb = rsb_all + P::RSB * gr.id;
   gr.scr = P::SCR ? scr_all + (size_t)P::SCR * gr.id : nullptr;
+  gr.prof = (prof && blockIdx.x == 0 && gr.id == 0 && gr.rank == 0) ? prof : nullptr;
   auto slot_at = [&](int d) {
     Slot sl;
     double* base = smem + ((size_t)gr.id * P::DB + (d % P::DB)) * P::SLOT;
@@ -831,6 +1092,7 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
     const long long off = prob * NN;
     const long long nxt = prob + stride;
     Slot s = slot_at(cur);
+    const long long tw0 = clock64();
     if constexpr (P::DB == 2) {
       if (nxt < batch) {
         issue_loads<EQ, N, G>(slot_at(cur ^ 1), in0, in1, in2, nxt * NN, gr.rank);
@@ -851,7 +1113,14 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
       s.p[2] = const_cast<double*>(in1) + off;
     }
     int flag = 0;
+    const long long tw1 = clock64();
+    if (gr.prof) gr.prof[0] += tw1 - tw0;  // wait for this problem's tiles
     run_variant<EQ, N, B, WG>(VAR{}, s, &flag, gr);
+    const long long tw2 = clock64();
+    if (gr.prof) {
+      gr.prof[1] += tw2 - tw1;  // compute
+      gr.prof[3] += 1;          // problems
+    }
     const bool fin = store_x<EQ, typename E::M0, N, G>(X + off, s.p[0], gr.rank);
     const bool allfin = __all_sync(0xffffffffu, fin);
     if (gr.wig == 0 && lane == 0 && flag) gflag[gr.id] = flag;
@@ -861,6 +1130,7 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
       const int f = gflag[gr.id];
       info[prob] = f ? f : (gbad[gr.id] ? -1 : 0);
     }
+    if (gr.prof) gr.prof[2] += clock64() - tw2;  // store + guards
     if constexpr (P::DB == 1) {
       gsync<WG>(gr);  // slot reads done before it is refilled
       if (nxt < batch) issue_loads<EQ, N, G>(slot_at(0), in0, in1, in2, nxt * NN, gr.rank);

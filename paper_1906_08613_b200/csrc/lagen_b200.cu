@@ -221,6 +221,12 @@ int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b
 
 int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                               const double* const* inputs, double* X, int* info, void* stream, int engine) {
+  return lagen_b200_execute_profile(eq, stmts, nstmts, n, b, batch, inputs, X, info, stream, engine, nullptr);
+}
+
+int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
+                               const double* const* inputs, double* X, int* info, void* stream, int engine,
+                               unsigned long long* d_prof) {
   if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_COLUMN) return fail(LAGEN_EINVAL, "unknown engine");
   int rc = check_common(eq, n, b, batch);
   if (rc) return rc;
@@ -238,6 +244,7 @@ int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n
   a.X = X;
   a.info = info;
   a.batch = batch;
+  a.prof = d_prof;
   LaunchFn fn = find_entry(eq, n, b)->launch;
   if (engine != LAGEN_ENGINE_GENERIC) {
     const int v = match_builtin(eq, stmts, nstmts);

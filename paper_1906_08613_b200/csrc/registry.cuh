@@ -15,6 +15,7 @@ struct LaunchArgs {
   double* X;
   int* info;
   long long batch;
+  unsigned long long* prof;  // warp-engine cycle accounting (profiling only), usually null
 };
 
 typedef cudaError_t (*LaunchFn)(const LaunchArgs&, cudaStream_t);
