@@ -47,6 +47,7 @@ __device__ __forceinline__ int tile_off(int tbase, int key, int r, int c) {
 template <int T, int LY>
 struct TM {
   static constexpr bool GLOBAL = false;
+  static constexpr int LDN = 0;
   static constexpr int TILES = LY == DENSE ? T * T : T * (T + 1) / 2;
   static constexpr int DOUBLES = TILES * 16;
   __device__ static __forceinline__ int tidx(int R, int C) {
@@ -70,6 +71,7 @@ struct TM {
 template <int N>
 struct GM {
   static constexpr bool GLOBAL = true;
+  static constexpr int LDN = N;
   static constexpr int TILES = 0;
   static constexpr int DOUBLES = 0;
   __device__ static __forceinline__ int off(int r, int c) { return r * N + c; }
@@ -565,91 +567,293 @@ __device__ __forceinline__ void chol_leaf_reg(const XV& W, int base, int* flag, 
 // push the fresh tiles' rank-4 contributions into later tiles of the same
 // tile-row / tile-column.
 // ----------------------------------------------------------------------------
+// whole 4x4 tiles of a matrix / view (tiled: 8 x 16-byte chunks; global:
+// 4 rows of 32 bytes), in view orientation
+template <class M>
+__device__ __forceinline__ void mat_tile_load(const double* base, int R, int C, double t[4][4]) {
+  if constexpr (M::GLOBAL) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const double2* p = reinterpret_cast<const double2*>(base + (4 * R + r) * M::LDN + 4 * C);
+      const double2 a = p[0], b = p[1];
+      t[r][0] = a.x;
+      t[r][1] = a.y;
+      t[r][2] = b.x;
+      t[r][3] = b.y;
+    }
+  } else {
+    const int tb = M::tidx(R, C) << 4, key = (R ^ C) & 7;
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch) {
+      const double2 v = *reinterpret_cast<const double2*>(base + tb + (((ch ^ key) & 7) << 1));
+      t[ch >> 1][2 * (ch & 1)] = v.x;
+      t[ch >> 1][2 * (ch & 1) + 1] = v.y;
+    }
+  }
+}
+template <class V>
+__device__ __forceinline__ void view_tile_load(const V& v, int I, int J, double t[4][4]) {
+  using M = typename V::Mat;
+  if constexpr (!V::tr) {
+    mat_tile_load<M>(v.base, (v.r0 >> 2) + I, (v.c0 >> 2) + J, t);
+  } else {
+    double u[4][4];
+    mat_tile_load<M>(v.base, (v.r0 >> 2) + J, (v.c0 >> 2) + I, u);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) t[a][b] = u[b][a];
+  }
+}
+template <class V>
+__device__ __forceinline__ void view_tile_store(const V& v, int I, int J, const double t[4][4]) {
+  using M = typename V::Mat;
+  static_assert(!V::tr && !M::GLOBAL, "stores go to the tiled unknown");
+  const int R = (v.r0 >> 2) + I, C = (v.c0 >> 2) + J;
+  const int tb = M::tidx(R, C) << 4, key = (R ^ C) & 7;
+#pragma unroll
+  for (int ch = 0; ch < 8; ++ch)
+    *reinterpret_cast<double2*>(v.base + tb + (((ch ^ key) & 7) << 1)) =
+        make_double2(t[ch >> 1][2 * (ch & 1)], t[ch >> 1][2 * (ch & 1) + 1]);
+}
+
+// one 4x4 tile of SYLV (reference column/row order inside the tile,
+// kernels.py:100-110), reciprocal shifted pivots off the substitution chain
 template <class LV, class UV, class WV>
-__device__ __forceinline__ void sylv_tile(const LV& Lv, const UV& Uv, const WV& W, int i0, int j0) {
-  double w[4][4];
+__device__ __forceinline__ void sylv_tile(const LV& Lv, const UV& Uv, const WV& W, int I, int J) {
+  double w[4][4], l[4][4], u[4][4];
+  view_tile_load(W, I, J, w);
+  view_tile_load(Lv, I, I, l);
+  view_tile_load(Uv, J, J, u);
+  double rp[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) w[a][b] = W.at(i0 + a, j0 + b);
-  // reciprocal shifted pivots 1 / (l_aa + u_bb): 16 independent divisions
-  // off the substitution chain (<= 1 ulp from the reference's division)
-  double rp[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const double laa = Lv.at(i0 + a, i0 + a);
-#pragma unroll
-    for (int b = 0; b < 4; ++b) rp[a][b] = 1.0 / (laa + Uv.at(j0 + b, j0 + b));
-  }
+    for (int b = 0; b < 4; ++b) rp[a][b] = 1.0 / (l[a][a] + u[b][b]);
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       double acc = 0.0;
 #pragma unroll
-      for (int c = 0; c < b; ++c) acc = fma(w[a][c], Uv.at(j0 + c, j0 + b), acc);
+      for (int c = 0; c < b; ++c) acc = fma(w[a][c], u[c][b], acc);
       w[a][b] -= acc;
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       double acc = 0.0;
 #pragma unroll
-      for (int c = 0; c < a; ++c) acc = fma(Lv.at(i0 + a, i0 + c), w[c][b], acc);
+      for (int c = 0; c < a; ++c) acc = fma(l[a][c], w[c][b], acc);
       w[a][b] = (w[a][b] - acc) * rp[a][b];
     }
   }
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) W.ref(i0 + a, j0 + b) = w[a][b];
+  view_tile_store(W, I, J, w);
 }
 
+// SYLV: L W + W U = W0, L (m x m) lower, U (q x q) upper [kernels.py:100-110]
+// 4x4-tile anti-diagonal wavefront: the tiles of anti-diagonal d are solved
+// (one thread each), then every later tile of the same tile-row / tile-column
+// receives the rank-4 contributions of the fresh tiles (one thread per
+// target tile, whole-tile loads).
 template <int WG, class LV, class UV, class WV>
 __device__ __forceinline__ void sylv(const LV& Lv, const UV& Uv, const WV& W, int m, int q, const Grp& gr) {
-  const int lane = gr.rank;
+  const int rank = gr.rank;
   constexpr int G = 32 * WG;
   const int TI = m >> 2, TJ = q >> 2;
+  const int ntile = TI * TJ;
+  // step d: every tile not yet solved takes the rank-4 contributions of the
+  // tiles solved at step d-1 in its tile-row / tile-column, and the tiles of
+  // anti-diagonal d are then solved by the thread that owns them — one group
+  // barrier per step.
   for (int d = 0; d <= TI + TJ - 2; ++d) {
-    const int ilo = d - (TJ - 1) > 0 ? d - (TJ - 1) : 0;
-    const int ihi = d < TI - 1 ? d : TI - 1;
-    for (int t = ilo + lane; t <= ihi; t += G) sylv_tile(Lv, Uv, W, 4 * t, 4 * (d - t));
-    if (d == TI + TJ - 2) break;
-    gsync<WG>(gr);
-    const int units = TI * TJ * 4;
-    for (int u = lane; u < units; u += G) {
-      const int tile = u >> 2, a = u & 3;
+    for (int tile = rank; tile < ntile; tile += G) {
       const int I2 = tile / TJ, J2 = tile - I2 * TJ;
-      if (I2 + J2 <= d) continue;
-      const int I1 = d - J2, J1 = d - I2;
-      const bool colc = (I1 >= 0 && I1 < I2);
-      const bool rowc = (J1 >= 0 && J1 < J2);
-      if (!colc && !rowc) continue;
-      const int i = 4 * I2 + a;
-      double l4[4] = {0, 0, 0, 0}, x4[4] = {0, 0, 0, 0};
+      if (I2 + J2 < d) continue;
+      const int I1 = d - 1 - J2, J1 = d - 1 - I2;
+      const bool colc = (d > 0 && I1 >= 0 && I1 < I2);
+      const bool rowc = (d > 0 && J1 >= 0 && J1 < J2);
+      const bool solve = (I2 + J2 == d);
+      if (!colc && !rowc && !solve) continue;
+      double w[4][4], a[4][4], x[4][4];
+      view_tile_load(W, I2, J2, w);
       if (colc) {
+        view_tile_load(Lv, I2, I1, a);
+        view_tile_load(W, I1, J2, x);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) l4[c] = Lv.at(i, 4 * I1 + c);
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sacc = fma(a[r][k], x[k][c], sacc);
+            w[r][c] -= sacc;
+          }
       }
       if (rowc) {
+        view_tile_load(W, I2, J1, x);
+        view_tile_load(Uv, J1, J2, a);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) x4[c] = W.at(i, 4 * J1 + c);
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sacc = fma(x[r][k], a[k][c], sacc);
+            w[r][c] -= sacc;
+          }
       }
+      if (solve) {
+        double l[4][4], u[4][4], rp[4][4];
+        view_tile_load(Lv, I2, I2, l);
+        view_tile_load(Uv, J2, J2, u);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int j = 4 * J2 + b;
-        double s = 0.0;
-        if (colc) {
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) s = fma(l4[c], W.at(4 * I1 + c, j), s);
+          for (int c = 0; c < 4; ++c) rp[r][c] = 1.0 / (l[r][r] + u[c][c]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < c; ++k) acc = fma(w[r][k], u[k][c], acc);
+            w[r][c] -= acc;
+          }
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < r; ++k) acc = fma(l[r][k], w[k][c], acc);
+            w[r][c] = (w[r][c] - acc) * rp[r][c];
+          }
         }
-        if (rowc) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) s = fma(x4[c], Uv.at(4 * J1 + c, j), s);
-        }
-        W.ref(i, j) -= s;
       }
+      view_tile_store(W, I2, J2, w);
     }
     gsync<WG>(gr);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// B <= 8 diagonal-block leaves in registers, run by one warp (lane 0 stores):
+// LYAP (kernels.py:113-130, reference (j, i <= j) order) and SYLV
+// (kernels.py:100-110, column-then-row order).
+// ----------------------------------------------------------------------------
+template <int B, class LV, class WV>
+__device__ __forceinline__ void lyap_leaf_reg(const LV& Lv, const WV& W) {
+  constexpr int TB = B / 4;
+  double l[B][B], x[B][B];
+#pragma unroll
+  for (int I = 0; I < TB; ++I)
+#pragma unroll
+    for (int J = 0; J < TB; ++J) {
+      double t[4][4];
+      if (J <= I) {
+        view_tile_load(Lv, I, J, t);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) l[4 * I + a][4 * J + b] = t[a][b];
+      }
+      if (I <= J) {
+        view_tile_load(W, I, J, t);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) x[4 * I + a][4 * J + b] = t[a][b];
+      }
+    }
+#pragma unroll
+  for (int j = 0; j < B; ++j)
+#pragma unroll
+    for (int i = 0; i <= j; ++i) {
+      const double rp = 1.0 / (l[i][i] + l[j][j]);
+      double acc = x[i][j], d1 = 0.0, d2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < i; ++q) d1 = fma(l[i][q], x[q][j], d1);
+#pragma unroll
+      for (int q = 0; q < j; ++q) d2 = fma(q < i ? x[q][i] : x[i][q], l[j][q], d2);
+      acc -= d1;
+      acc -= d2;
+      x[i][j] = acc * rp;
+    }
+  if (lane_id() == 0) {
+#pragma unroll
+    for (int I = 0; I < TB; ++I)
+#pragma unroll
+      for (int J = I; J < TB; ++J) {
+        double t[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int r = 4 * I + a, c = 4 * J + b;
+            t[a][b] = r <= c ? x[r][c] : x[c][r];
+          }
+        view_tile_store(W, I, J, t);
+      }
+  }
+}
+
+template <int B, class LV, class UV, class WV>
+__device__ __forceinline__ void sylv_leaf_reg(const LV& Lv, const UV& Uv, const WV& W) {
+  constexpr int TB = B / 4;
+  double l[B][B], u[B][B], x[B][B];
+#pragma unroll
+  for (int I = 0; I < TB; ++I)
+#pragma unroll
+    for (int J = 0; J < TB; ++J) {
+      double t[4][4];
+      view_tile_load(W, I, J, t);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) x[4 * I + a][4 * J + b] = t[a][b];
+      if (J <= I) {
+        view_tile_load(Lv, I, J, t);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) l[4 * I + a][4 * J + b] = t[a][b];
+      }
+      if (I <= J) {
+        view_tile_load(Uv, I, J, t);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) u[4 * I + a][4 * J + b] = t[a][b];
+      }
+    }
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < j; ++c) acc = fma(x[i][c], u[c][j], acc);
+      x[i][j] -= acc;
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const double rp = 1.0 / (l[i][i] + u[j][j]);
+      double acc = 0.0;
+#pragma unroll
+      for (int c = 0; c < i; ++c) acc = fma(l[i][c], x[c][j], acc);
+      x[i][j] = (x[i][j] - acc) * rp;
+    }
+  }
+  if (lane_id() == 0) {
+#pragma unroll
+    for (int I = 0; I < TB; ++I)
+#pragma unroll
+      for (int J = 0; J < TB; ++J) {
+        double t[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) t[a][b] = x[4 * I + a][4 * J + b];
+        view_tile_store(W, I, J, t);
+      }
   }
 }
 
@@ -798,12 +1002,20 @@ __device__ __forceinline__ void exec(const Slot& s, const Rep<N, B>& rp, int* fl
     using Bv = typename S::in1;
     const auto Lv = mkv<E, A, false>(s, rp.st(A::r), rp.st(A::c));
     const auto Uv = mkv<E, Bv, false>(s, rp.st(Bv::r), rp.st(Bv::c));
-    sylv<WG>(Lv, Uv, Ov, m, q, gr);
+    if constexpr (O::r == O::c && B <= 4) {
+      if (gr.wig == 0) sylv_leaf_reg<B>(Lv, Uv, Ov);  // m == q == B
+    } else {
+      sylv<WG>(Lv, Uv, Ov, m, q, gr);
+    }
   } else if constexpr (S::kind == K_LYAP) {
     using A = typename S::in0;
     const auto Lv = mkv<E, A, false>(s, rp.st(A::r), rp.st(A::c));
     const auto Ws = mkv<E, O, true>(s, rp.st(O::r), rp.st(O::c));
-    lyap<WG>(Lv, Ov, Ws, m, gr);
+    if constexpr (B <= 8) {
+      if (gr.wig == 0) lyap_leaf_reg<B>(Lv, Ov);
+    } else {
+      lyap<WG>(Lv, Ov, Ws, m, gr);
+    }
   }
 }
 
@@ -833,11 +1045,15 @@ constexpr bool sd_reads(const SD& a, int op, int r, int c) {
 constexpr bool sd_dep(const SD& a, const SD& b) {  // b (later) depends on a
   return sd_reads(b, a.oop, a.orr, a.oc) || sd_reads(a, b.oop, b.orr, b.oc);
 }
-template <int M>
+template <int M, int B>
 struct Sched {
   int level[M > 0 ? M : 1];
   int nlevels;
   int leaf_level_has_leaf[M > 0 ? M : 1];
+  // single-warp statements: CHOL leaves, and LYAP / diagonal SYLV leaves for B <= 8
+  static constexpr bool is_leaf(const SD& s) {
+    return s.kind == K_CHOL || (B <= 8 && s.kind == K_LYAP) || (B <= 4 && s.kind == K_SYLV && s.orr == s.oc);
+  }
   constexpr Sched(const SD* d) : level{}, nlevels(0), leaf_level_has_leaf{} {
     int asap[M > 0 ? M : 1] = {};
     for (int j = 0; j < M; ++j) {
@@ -858,21 +1074,21 @@ struct Sched {
     nlevels = depth;
     for (int j = 0; j < M; ++j) leaf_level_has_leaf[j] = 0;
     for (int j = 0; j < M; ++j)
-      if (d[j].kind == K_CHOL) leaf_level_has_leaf[level[j]] = 1;
+      if (is_leaf(d[j])) leaf_level_has_leaf[level[j]] = 1;
   }
 };
 
-template <class... S>
+template <int B, class... S>
 struct VarInfo {
   static constexpr int M = sizeof...(S);
   static constexpr SD d[M] = {make_sd<S>()...};
-  static constexpr Sched<M> sch{d};
+  static constexpr Sched<M, B> sch{d};
 };
 
 template <int EQ, int N, int B, int WG, int L, class INFO, class S, int I>
 __device__ __forceinline__ void exec_if(const Slot& s, const Rep<N, B>& rp, int* flag, const Grp& gr) {
   if constexpr (INFO::sch.level[I] == L) {
-    constexpr bool shared_level = (WG > 1) && INFO::sch.leaf_level_has_leaf[L] && S::kind != K_CHOL;
+    constexpr bool shared_level = (WG > 1) && INFO::sch.leaf_level_has_leaf[L] && !INFO::sch.is_leaf(make_sd<S>());
     Sub sb;
     if constexpr (shared_level) {
       if (gr.wig == 0) return;  // warp 0 runs the leaf of this level
@@ -913,7 +1129,7 @@ __device__ __forceinline__ void run_iter(const Slot& s, const Rep<N, B>& rp, int
 
 template <int EQ, int N, int B, int WG, class... S>
 __device__ __forceinline__ void run_variant(Var<S...>, const Slot& s, int* flag, const Grp& gr) {
-  using INFO = VarInfo<S...>;
+  using INFO = VarInfo<B, S...>;
 #pragma unroll 1
   for (int k = 0; k < N / B; ++k) {
     Rep<N, B> rp{k};
