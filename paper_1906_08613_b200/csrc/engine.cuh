@@ -544,19 +544,40 @@ __device__ __forceinline__ void chol_leaf_reg(const XV& W, int base, int* flag, 
 #pragma unroll
       for (int c = r; c < B; ++c) t[r][c] = fma(-t[i][r], t[i][c], t[r][c]);
   }
-  if (lane == 0) {
-    if (bad && *flag == 0) *flag = base + badi + 1;
-    // factor back into the tiles (upper elements only), the row-major
-    // factor and the reciprocal pivots for this iteration's TRSM
+  if (lane == 0 && bad && *flag == 0) *flag = base + badi + 1;
+  // lane r < B takes row r of the (lane-uniform) factor with selects (no
+  // branches) and stores it: into the tiles (upper part), the row-major
+  // factor and the reciprocal pivot for this iteration's TRSM — B lanes store
+  // in parallel instead of one lane storing everything
+  double row[B];
+  double rsr = 0.0;
+#pragma unroll
+  for (int c = 0; c < B; ++c) row[c] = 0.0;
+#pragma unroll
+  for (int r = 0; r < B; ++r) {
+    const bool me = (lane == r);
+#pragma unroll
+    for (int c = r; c < B; ++c) row[c] = me ? t[r][c] : row[c];
+    rsr = me ? rs[r] : rsr;
+  }
+  if (lane < B) {
+    const int r = lane;
+    const int R = K + (r >> 2);
+    int tbr[TB], kyr[TB];
+#pragma unroll
+    for (int J = 0; J < TB; ++J) {
+      const int C = K + J;
+      tbr[J] = (C >= R) ? (M::tidx(R, C) << 4) : 0;
+      kyr[J] = (R ^ C) & 7;
+    }
 #pragma unroll
     for (int c = 0; c < B; ++c) {
-#pragma unroll
-      for (int r = 0; r <= c; ++r) {
-        W.base[tile_off(tb[r / 4][c / 4], ky[r / 4][c / 4], r, c)] = t[r][c];
-        rsb[16 + r * B + c] = t[r][c];
+      if (c >= r) {
+        W.base[tile_off(tbr[c / 4], kyr[c / 4], r, c)] = row[c];
+        rsb[16 + r * B + c] = row[c];
       }
-      rsb[c] = rs[c];
     }
+    rsb[r] = rsr;
   }
 }
 
