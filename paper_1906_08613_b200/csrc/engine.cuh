@@ -311,9 +311,58 @@ __device__ __forceinline__ void gemm_row8(const OV& O, const AV& A, const BV& Bm
   }
 }
 
+// single 8x8 output tile (m, q <= 8) on one warp: four independent
+// accumulator chains over the k-steps (latency-bound otherwise)
+template <bool UP, class OV, class AV, class BV>
+__device__ __forceinline__ void gemm_tile8(const OV& O, const AV& A, const BV& Bm, int m, int p, int q, double sgn) {
+  const int lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int ra = (g < m) ? g : (g & 3);
+  const int cb = (g < q) ? g : (g & 3);
+  AStream<AV> as;
+  BStream<BV> bs;
+  as.init(A, ra, 0);
+  bs.init(Bm, cb, 0);
+  double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
+  int k0 = 0;
+  for (; k0 + 16 <= p; k0 += 16) {
+    double a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = as.load(A.base);
+      b[u] = bs.load(Bm.base);
+      as.step();
+      bs.step();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(c0[u], c1[u], a[u], b[u]);
+  }
+  for (int u = 0; k0 < p; k0 += 4, ++u) {
+    const double a = as.load(A.base), b = bs.load(Bm.base);
+    as.step();
+    bs.step();
+    dmma(c0[0], c1[0], a, b);
+  }
+  const double x0 = (c0[0] + c0[1]) + (c0[2] + c0[3]);
+  const double x1 = (c1[0] + c1[1]) + (c1[2] + c1[3]);
+  const int i = g, j = 2 * t;
+  if (i < m && j < q && (!UP || i <= j)) {
+    double& o0 = O.ref(i, j);
+    o0 = fma(sgn, x0, o0);
+  }
+  if (i < m && j + 1 < q && (!UP || i <= j + 1)) {
+    double& o1 = O.ref(i, j + 1);
+    o1 = fma(sgn, x1, o1);
+  }
+}
+
 template <bool UP, int WG, class OV, class AV, class BV>
 __device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int m, int p, int q, double sgn,
                                      const Grp& gr, const Sub& sb) {
+  if (m <= 8 && q <= 8 && !(sb.full && WG > 1)) {
+    if (sb.w == 0) gemm_tile8<UP>(O, A, Bm, m, p, q, sgn);
+    return;
+  }
   if (m <= 8 && q > 8) {
     gemm_row8<UP>(O, A, Bm, m, p, q, sgn, sb);
     return;
@@ -570,12 +619,12 @@ __device__ __forceinline__ void chol_leaf_reg(const XV& W, int base, int* flag, 
       tbr[J] = (C >= R) ? (M::tidx(R, C) << 4) : 0;
       kyr[J] = (R ^ C) & 7;
     }
+    // whole rows (zeros left of the diagonal): only the tile-level predicate
+    // remains, so the stores need no divergent branches
 #pragma unroll
     for (int c = 0; c < B; ++c) {
-      if (c >= r) {
-        W.base[tile_off(tbr[c / 4], kyr[c / 4], r, c)] = row[c];
-        rsb[16 + r * B + c] = row[c];
-      }
+      rsb[16 + r * B + c] = row[c];
+      if ((c >> 2) >= (r >> 2)) W.base[tile_off(tbr[c / 4], kyr[c / 4], r, c)] = row[c];
     }
     rsb[r] = rsr;
   }
@@ -1071,6 +1120,7 @@ struct Sched {
   int level[M > 0 ? M : 1];
   int nlevels;
   int leaf_level_has_leaf[M > 0 ? M : 1];
+  int prefix[M > 0 ? M : 1];  // GEMM updates of a leaf's block run by the leaf warp right before it
   // single-warp statements: CHOL leaves, and LYAP / diagonal SYLV leaves for B <= 8
   static constexpr bool is_leaf(const SD& s) {
     return s.kind == K_CHOL || (B <= 8 && s.kind == K_LYAP) || (B <= 4 && s.kind == K_SYLV && s.orr == s.oc);
@@ -1093,6 +1143,37 @@ struct Sched {
       level[j] = l;
     }
     nlevels = depth;
+    // leaf prefixes: a GEMM whose output is a leaf's block and that nothing
+    // but the leaf depends on moves into the leaf's level, executed by the
+    // leaf warp right before the leaf (no group barrier in between)
+    for (int j = 0; j < M; ++j) prefix[j] = 0;
+    for (int l = 0; l < M; ++l) {
+      if (!is_leaf(d[l])) continue;
+      for (int j = 0; j < l; ++j) {
+        if (d[j].kind != K_GEMM || d[j].orr != d[l].orr || d[j].oc != d[l].oc || d[j].oop != d[l].oop) continue;
+        bool only_leaf = true;
+        for (int k = j + 1; k < M; ++k)
+          if (k != l && sd_dep(d[j], d[k]) && level[k] <= level[l] &&
+              !(d[k].kind == K_GEMM && d[k].orr == d[l].orr && d[k].oc == d[l].oc))
+            only_leaf = false;  // a dependent that would run no later than the leaf
+        if (only_leaf) {
+          prefix[j] = 1;
+          level[j] = level[l];
+        }
+      }
+    }
+    // compact the level numbers (a level may have emptied)
+    int remap[M > 0 ? M : 1] = {};
+    for (int L = 0; L < M; ++L) remap[L] = -1;
+    int nl = 0;
+    for (int L = 0; L < depth; ++L) {
+      bool used = false;
+      for (int j = 0; j < M; ++j)
+        if (level[j] == L) used = true;
+      if (used) remap[L] = nl++;
+    }
+    for (int j = 0; j < M; ++j) level[j] = remap[level[j]];
+    nlevels = nl;
     for (int j = 0; j < M; ++j) leaf_level_has_leaf[j] = 0;
     for (int j = 0; j < M; ++j)
       if (is_leaf(d[j])) leaf_level_has_leaf[level[j]] = 1;
@@ -1109,9 +1190,18 @@ struct VarInfo {
 template <int EQ, int N, int B, int WG, int L, class INFO, class S, int I>
 __device__ __forceinline__ void exec_if(const Slot& s, const Rep<N, B>& rp, int* flag, const Grp& gr) {
   if constexpr (INFO::sch.level[I] == L) {
-    constexpr bool shared_level = (WG > 1) && INFO::sch.leaf_level_has_leaf[L] && !INFO::sch.is_leaf(make_sd<S>());
+    constexpr bool is_prefix = INFO::sch.prefix[I] != 0;
+    constexpr bool shared_level =
+        (WG > 1) && INFO::sch.leaf_level_has_leaf[L] && !INFO::sch.is_leaf(make_sd<S>()) && !is_prefix;
     Sub sb;
-    if constexpr (shared_level) {
+    if constexpr (is_prefix && WG > 1) {
+      if (gr.wig != 0) return;  // the leaf warp runs its block's updates
+      sb.w = 0;
+      sb.nw = 1;
+      sb.rank = gr.rank;
+      sb.nthr = 32;
+      sb.full = false;
+    } else if constexpr (shared_level) {
       if (gr.wig == 0) return;  // warp 0 runs the leaf of this level
       sb.w = gr.wig - 1;
       sb.nw = WG - 1;
@@ -1148,15 +1238,60 @@ __device__ __forceinline__ void run_iter(const Slot& s, const Rep<N, B>& rp, int
   (run_level<EQ, N, B, WG, Ls, INFO, S...>(s, rp, flag, gr, std::index_sequence_for<S...>{}), ...);
 }
 
+// Cholesky variants whose iteration k finalises block row k (those with an
+// "X12 := ..." statement: v1, v2) stream that block row to HBM right after
+// the iteration, overlapping the output writes with later iterations.
+template <class... S>
+struct RowFinal {
+  static constexpr bool value = ((S::out::r == 1 && S::out::c == 2) || ...);
+};
+
+template <int N, class M, int G>
+__device__ __forceinline__ bool store_chol_rows(double* __restrict__ dst, const double* xs, int r0, int r1, int rank) {
+  constexpr int T = N / 4;
+  bool finite = true;
+  const int units = (r1 - r0) * T;  // (row, tile column) units of 4 doubles
+  for (int u = rank; u < units; u += G) {
+    const int r = r0 + u / T, C = u % T, c = 4 * C, R = r >> 2;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    if (C >= R) {
+      const double2 p0 = *reinterpret_cast<const double2*>(xs + M::off(r, c));
+      const double2 p1 = *reinterpret_cast<const double2*>(xs + M::off(r, c + 2));
+      v[0] = (c >= r) ? p0.x : 0.0;
+      v[1] = (c + 1 >= r) ? p0.y : 0.0;
+      v[2] = (c + 2 >= r) ? p1.x : 0.0;
+      v[3] = (c + 3 >= r) ? p1.y : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) finite = finite && isfinite(v[e]);
+    double2* gp = reinterpret_cast<double2*>(dst + r * N + c);
+    __stcs(gp, make_double2(v[0], v[1]));
+    __stcs(gp + 1, make_double2(v[2], v[3]));
+  }
+  return finite;
+}
+
 template <int EQ, int N, int B, int WG, class... S>
-__device__ __forceinline__ void run_variant(Var<S...>, const Slot& s, int* flag, const Grp& gr) {
+__device__ __forceinline__ bool run_variant(Var<S...>, const Slot& s, int* flag, const Grp& gr, double* xout) {
   using INFO = VarInfo<B, S...>;
+  bool finite = true;
 #pragma unroll 1
   for (int k = 0; k < N / B; ++k) {
     Rep<N, B> rp{k};
     run_iter<EQ, N, B, WG, INFO, S...>(s, rp, flag, gr, std::make_integer_sequence<int, INFO::sch.nlevels>{});
+    if constexpr (EQ == 0 && RowFinal<S...>::value)
+      finite = store_chol_rows<N, typename EqT<EQ, N>::M0, 32 * WG>(xout, s.p[0], k * B, (k + 1) * B, gr.rank) &&
+               finite;
   }
+  return finite;
 }
+
+template <class VAR>
+struct StreamsRows;
+template <class... S>
+struct StreamsRows<Var<S...>> {
+  static constexpr bool value = RowFinal<S...>::value;
+};
 
 // ----------------------------------------------------------------------------
 // global -> tiled shared memory (cp.async, 16 B chunks), one warp per problem
@@ -1352,13 +1487,14 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
     int flag = 0;
     const long long tw1 = clock64();
     if (gr.prof) gr.prof[0] += tw1 - tw0;  // wait for this problem's tiles
-    run_variant<EQ, N, B, WG>(VAR{}, s, &flag, gr);
+    bool fin = run_variant<EQ, N, B, WG>(VAR{}, s, &flag, gr, X + off);
     const long long tw2 = clock64();
     if (gr.prof) {
       gr.prof[1] += tw2 - tw1;  // compute
       gr.prof[3] += 1;          // problems
     }
-    const bool fin = store_x<EQ, typename E::M0, N, G>(X + off, s.p[0], gr.rank);
+    if constexpr (!(EQ == 0 && StreamsRows<VAR>::value))
+      fin = store_x<EQ, typename E::M0, N, G>(X + off, s.p[0], gr.rank) && fin;
     const bool allfin = __all_sync(0xffffffffu, fin);
     if (gr.wig == 0 && lane == 0 && flag) gflag[gr.id] = flag;
     if (lane == 0 && !allfin) atomicOr(&gbad[gr.id], 1);
