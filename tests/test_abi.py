@@ -98,3 +98,27 @@ def test_rejects_bad_arguments_without_a_device():
     assert _execute(0, v, 16, 4, 0) == 0              # empty batch is a no-op
     lyap = builtin_variants("lyapunov")[0].statements
     assert _execute(0, lyap, 16, 4, 1) == -3          # LYAP/SYLV inside Cholesky
+
+
+def test_dispatch_table_points_at_instantiated_kernels():
+    """Every autotuned (variant, b, engine) choice must exist in the library."""
+    import json
+    from paper_1906_08613_b200 import dispatch
+    table = json.loads(dispatch.TABLE.read_text())
+    assert set(table) == set(EQUATIONS)
+    for eq, entries in table.items():
+        assert len(entries) == 32, eq
+        for n, e in entries.items():
+            n = int(n)
+            assert e["b"] in default_blocks(n)
+            assert 0 <= e["variant"] < len(builtin_variants(eq))
+            assert _lib.engine_supported(EQ_CODES[eq], n, e["b"], e["variant"], e.get("engine", "generic")), (eq, n, e)
+
+
+def test_every_variant_has_a_generic_kernel_at_every_size():
+    """The generic engine covers the whole variant space (23 variants x default b x n)."""
+    for eq in EQUATIONS:
+        for n in range(4, 129, 4):
+            for b in default_blocks(n):
+                for v in builtin_variants(eq):
+                    assert _lib.engine_supported(EQ_CODES[eq], n, b, v.index, "generic")
