@@ -117,6 +117,12 @@ int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b
 #define LAGEN_ENGINE_GENERIC 1
 #define LAGEN_ENGINE_WARP 2
 #define LAGEN_ENGINE_COLUMN 3
+/* 4x4-tile task DAG (right-looking variants, b <= 8): tasks of successive
+ * iterations overlap as soon as their input tiles are final */
+#define LAGEN_ENGINE_DATAFLOW 4
+/* Cholesky v1 on a packed row-major upper layout (cheap DMMA operand
+ * addressing for the block-row updates) */
+#define LAGEN_ENGINE_ROWS 5
 int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
                               long long batch, const double* const* inputs, double* X,
                               int* info, void* stream, int engine);

@@ -47,6 +47,18 @@ def _stale(target, deps):
     return any(d.stat().st_mtime > t for d in deps)
 
 
+def _deps(src, obj, headers):
+    """Headers src includes, from the nvcc -MD file of its last compile (all
+    headers when unknown)."""
+    dfile = obj.with_suffix(".d")
+    if not dfile.exists():
+        return headers
+    text = dfile.read_text().replace("\\\n", " ")
+    names = text.split(":", 1)[1].split() if ":" in text else []
+    deps = [Path(n) for n in names if n.endswith((".cuh", ".h")) and str(REPO) in str(Path(n).resolve())]
+    return [d for d in deps if d.exists()] + [h for h in headers if h.name == "lagen_b200.h"]
+
+
 def build(force=False, verbose=False, jobs=None):
     sources = sorted(CSRC.glob("*.cu"))
     if not sources:
@@ -58,13 +70,14 @@ def build(force=False, verbose=False, jobs=None):
     for src in sources:
         obj = OBJ / (src.stem + ".o")
         objs.append(obj)
-        if force or _stale(obj, [src] + headers):
+        if force or _stale(obj, [src] + _deps(src, obj, headers)):
             todo.append((src, obj))
     cc = nvcc()
 
     def compile_one(item):
         src, obj = item
-        cmd = [cc, *ARCH, *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src), "-o", str(obj)]
+        cmd = [cc, *ARCH, *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-MD", "-MF", str(obj.with_suffix(".d")),
+               "-c", str(src), "-o", str(obj)]
         proc = subprocess.run(cmd, capture_output=True, text=True)
         if proc.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src.name}:\n{proc.stderr}")

@@ -1,0 +1,437 @@
+// chol_rows.cuh — the "rows engine": Cholesky variant v1 on a packed
+// row-major upper layout.
+//
+// Variant v1 (the reference's enumeration, variants_table.json):
+//     S1: X11 -= X01^T X01      (upper target)
+//     S2: X11 := CHOL(X11)
+//     S3: X12 -= X01^T X02
+//     S4: X12 := TRSM(X11^T, X12)                 (verify.py:245-297)
+// Both GEMM operands are segments of the rows above the current block row,
+// so X lives in shared memory as its upper rows, row-major: row r keeps
+// columns [4*floor(r/4), n) (16-byte aligned).  The m8n8k4 DMMA fragments of
+// one k-step (4 rows) are then addressed from one per-lane row pointer that
+// advances with two integer ops (the tiled layout of the generic engines
+// spends ~35% of its instructions on address arithmetic here, measured).
+//
+// Schedule per iteration (group of WG warps owns a problem, P problems per
+// CTA as the warp engine's WPolicy):
+//   level A  warp 0: S1 (one 8x8 DMMA tile, 4 accumulator chains), then the
+//            CHOL leaf in registers (rsqrt pivots; reciprocals + factor to
+//            rsb for S4); warps 1..WG-1 concurrently: S3 in 8x32 DMMA blocks,
+//            k split across idle warps with a fixed-order reduction
+//   level B  all: S4, lanes own columns
+//   then     block row k streams to HBM (zeros left of the diagonal)
+// Per element the arithmetic is v1's statements (S3 does not depend on S2).
+#pragma once
+#include "engine.cuh"
+
+namespace lagen {
+namespace cr {
+
+using eng::cp_async16;
+using eng::cp_async_commit;
+using eng::cp_async_wait;
+using eng::dmma;
+using eng::Grp;
+using eng::gsync;
+using eng::lane_id;
+
+// packed upper rows: row r starts at column 4R (R = r / 4)
+template <int N>
+struct Rows {
+  static constexpr int DOUBLES = N * N / 2 + 2 * N;
+  __device__ static __forceinline__ int off(int r) {
+    const int R = r >> 2;
+    return 4 * N * R - 8 * R * (R - 1) + (r & 3) * (N - 4 * R);
+  }
+  // address of element (r, c), c >= 4 * floor(r / 4)
+  __device__ static __forceinline__ int at(int r, int c) { return off(r) + c - 4 * (r >> 2); }
+};
+
+// Row pointer of lane t for the k-step covering rows 4R' .. 4R'+3: element
+// (4R' + t, c) is at p + c.  step() moves to R' + 1.
+template <int N>
+struct KRow {
+  int p, d;
+  __device__ __forceinline__ void init(int t, int Rk) {
+    p = Rows<N>::off(4 * Rk + t) - 4 * Rk;
+    d = 4 * N - 4 - 4 * t - 16 * Rk;
+  }
+  __device__ __forceinline__ void step() {
+    p += d;
+    d -= 16;
+  }
+};
+
+// row-major n x n (upper part) -> packed rows, cp.async 16-byte units
+template <int N, int G>
+__device__ __forceinline__ void load_rows(double* xs, const double* __restrict__ src, int rank) {
+#pragma unroll 1
+  for (int R = 0; R < N / 4; ++R) {
+    const int per = (N - 4 * R) >> 1;  // units per row of group R
+    for (int u = rank; u < 4 * per; u += G) {
+      const int r = 4 * R + u / per, c = 4 * R + 2 * (u % per);
+      cp_async16(xs + Rows<N>::at(r, c), src + r * N + c);
+    }
+  }
+}
+
+// S1: X11 (B x B upper) -= X01^T X01, K = r0; one warp, 4 accumulator chains
+template <int N, int B>
+__device__ __forceinline__ void s1_tile(double* xs, int r0) {
+  const int lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int ga = (B == 8 || g < B) ? g : (g & 3);
+  double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
+  KRow<N> kr;
+  kr.init(t, 0);
+  const int nks = r0 >> 2;
+  int ks = 0;
+  for (; ks + 4 <= nks; ks += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = xs[kr.p + r0 + ga];
+      b[u] = xs[kr.p + r0 + (g & (B - 1))];
+      kr.step();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(c0[u], c1[u], a[u], b[u]);
+  }
+  for (int u = 0; ks < nks; ++ks, ++u) {
+    const double a = xs[kr.p + r0 + ga], b = xs[kr.p + r0 + (g & (B - 1))];
+    kr.step();
+    dmma(c0[u & 3], c1[u & 3], a, b);
+  }
+  const double x0 = (c0[0] + c0[1]) + (c0[2] + c0[3]);
+  const double x1 = (c1[0] + c1[1]) + (c1[2] + c1[3]);
+  const int i = g, j = 2 * t;
+  if (i < B && j < B) {
+    const int o = Rows<N>::at(r0 + i, r0 + j);
+    if (i <= j) xs[o] -= x0;
+    if (i <= j + 1 && j + 1 < B) xs[o + 1] -= x1;
+  }
+}
+
+// S3 block: rows r0..r0+B-1, columns [c0, c0 + 32) of X12 (absolute columns),
+// k-steps [ks0, ks1); accumulators returned (even / odd sets folded)
+template <int N, int B>
+__device__ __forceinline__ void s3_block(const double* xs, int r0, int c0, int cend, int ks0, int ks1, double c0a[4],
+                                         double c1a[4]) {
+  const int lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  const int ga = (B == 8 || g < B) ? g : (g & 3);
+  double e0[4] = {0, 0, 0, 0}, e1[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) c0a[u] = c1a[u] = 0.0;
+  bool v[4];
+  int cb[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int c = c0 + 8 * u + g;
+    v[u] = c < cend;
+    cb[u] = v[u] ? c : r0;  // clamped to a valid column (result discarded)
+  }
+  KRow<N> kr;
+  kr.init(t, ks0);
+  int ks = ks0;
+  for (; ks + 2 <= ks1; ks += 2) {
+    const double a = xs[kr.p + r0 + ga];
+    double bv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bv[u] = xs[kr.p + cb[u]];
+    kr.step();
+    const double a2 = xs[kr.p + r0 + ga];
+    double bw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bw[u] = xs[kr.p + cb[u]];
+    kr.step();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(c0a[u], c1a[u], a, bv[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(e0[u], e1[u], a2, bw[u]);
+  }
+  if (ks < ks1) {
+    const double a = xs[kr.p + r0 + ga];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(c0a[u], c1a[u], a, xs[kr.p + cb[u]]);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    c0a[u] += e0[u];
+    c1a[u] += e1[u];
+  }
+}
+
+template <int N, int B>
+__device__ __forceinline__ void s3_write(double* xs, int r0, int c0, int cend, const double c0a[4],
+                                         const double c1a[4]) {
+  const int lane = lane_id();
+  const int g = lane >> 2, t = lane & 3;
+  if (g >= B) return;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int c = c0 + 8 * u + 2 * t;
+    if (c < cend) {
+      double2* p = reinterpret_cast<double2*>(xs + Rows<N>::at(r0 + g, c));
+      double2 w = *p;
+      w.x -= c0a[u];
+      w.y -= c1a[u];
+      *p = w;
+    }
+  }
+}
+
+// S3 over warps [w0, w0 + nw) (wi = this warp's index in that set); k split
+// across idle warps, partials reduced in fixed order through scratch.
+template <int N, int B, int WG>
+__device__ __forceinline__ void s3(double* xs, int r0, int wi, int nw, const Grp& gr, int bar_id, int bar_thr) {
+  const int cs = r0 + B, cend = N;
+  if (cs >= cend || r0 == 0) return;
+  const int nblk = (cend - cs + 31) >> 5;
+  const int nks = r0 >> 2;
+  const int ks = (gr.scr != nullptr && nblk < nw) ? min(nw / nblk, nks / 4) : 1;
+  if (ks <= 1) {
+    for (int bk = wi; bk < nblk; bk += nw) {
+      double a0[4], a1[4];
+      s3_block<N, B>(xs, r0, cs + 32 * bk, cend, 0, nks, a0, a1);
+      s3_write<N, B>(xs, r0, cs + 32 * bk, cend, a0, a1);
+    }
+    return;
+  }
+  auto bar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_thr) : "memory"); };
+  const int blk = wi % nblk, sl = wi / nblk;
+  const bool active = wi < nblk * ks;
+  const int lane = lane_id();
+  double a0[4], a1[4];
+  if (active) {
+    s3_block<N, B>(xs, r0, cs + 32 * blk, cend, (nks * sl) / ks, (nks * (sl + 1)) / ks, a0, a1);
+    if (sl > 0) {
+      double* sp = gr.scr + ((sl - 1) * nblk + blk) * 256 + lane * 8;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        sp[2 * u] = a0[u];
+        sp[2 * u + 1] = a1[u];
+      }
+    }
+  }
+  bar();
+  if (active && sl == 0) {
+    for (int s2 = 1; s2 < ks; ++s2) {
+      const double* sp = gr.scr + ((s2 - 1) * nblk + blk) * 256 + lane * 8;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a0[u] += sp[2 * u];
+        a1[u] += sp[2 * u + 1];
+      }
+    }
+    s3_write<N, B>(xs, r0, cs + 32 * blk, cend, a0, a1);
+  }
+  bar();
+}
+
+// CHOL leaf (B <= 8) on one warp: every lane factors the block in registers;
+// lane r < B writes row r (zeros left of the diagonal), its reciprocal pivot
+// to rsb[r] and the factor row-major to rsb[16 + r * B + c].
+template <int N, int B>
+__device__ __forceinline__ void leaf(double* xs, int r0, double* rsb, int* flag) {
+  const int lane = lane_id();
+  double t[B][B];
+#pragma unroll
+  for (int r = 0; r < B; ++r) {
+    // row r0 + r is stored from column 4 * floor((r0 + r) / 4) = r0 + (r & ~3)
+    const int o = Rows<N>::at(r0 + r, r0 + (r & ~3));
+#pragma unroll
+    for (int c = 0; c < B; c += 2) {
+      if (c < (r & ~3)) {
+        t[r][c] = t[r][c + 1] = 0.0;
+        continue;
+      }
+      const double2 v = *reinterpret_cast<const double2*>(xs + o + c - (r & ~3));
+      t[r][c] = c >= r ? v.x : 0.0;
+      t[r][c + 1] = c + 1 >= r ? v.y : 0.0;
+    }
+  }
+  double rs[B];
+  bool bad = false;
+  int badi = 0;
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    const double piv = t[i][i];
+    if (!bad && piv <= 0.0) {
+      bad = true;
+      badi = i;
+    }
+    rs[i] = rsqrt(piv);
+    t[i][i] = piv * rs[i];
+#pragma unroll
+    for (int c = i + 1; c < B; ++c) t[i][c] *= rs[i];
+#pragma unroll
+    for (int r = i + 1; r < B; ++r)
+#pragma unroll
+      for (int c = r; c < B; ++c) t[r][c] = fma(-t[i][r], t[i][c], t[r][c]);
+  }
+  if (lane == 0 && bad && *flag == 0) *flag = r0 + badi + 1;
+  double row[B];
+  double rsr = 0.0;
+#pragma unroll
+  for (int c = 0; c < B; ++c) row[c] = 0.0;
+#pragma unroll
+  for (int r = 0; r < B; ++r) {
+    const bool me = lane == r;
+#pragma unroll
+    for (int c = r; c < B; ++c) row[c] = me ? t[r][c] : row[c];
+    rsr = me ? rs[r] : rsr;
+  }
+  if (lane < B) {
+    const int cs = lane & ~3;  // first stored column of this row (relative to r0)
+    const int o = Rows<N>::at(r0 + lane, r0 + cs);
+#pragma unroll
+    for (int c = 0; c < B; c += 2)
+      if (c >= cs) *reinterpret_cast<double2*>(xs + o + c - cs) = make_double2(row[c], row[c + 1]);
+#pragma unroll
+    for (int c = 0; c < B; ++c) rsb[16 + lane * B + c] = row[c];
+    rsb[lane] = rsr;
+  }
+}
+
+// S4: X12 := X11^{-T} X12, threads own columns
+template <int N, int B>
+__device__ __forceinline__ void trsm(double* xs, int r0, const double* rsb, int rank, int nthr) {
+  int o[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) o[i] = Rows<N>::at(r0 + i, 0);
+  for (int c = r0 + B + rank; c < N; c += nthr) {
+    double w[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) w[i] = xs[o[i] + c];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      double v = w[i];
+#pragma unroll
+      for (int l = 0; l < i; ++l) v = fma(-rsb[16 + l * B + i], w[l], v);
+      w[i] = v * rsb[i];
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i) xs[o[i] + c] = w[i];
+  }
+}
+
+// block row [r0, r0 + B) -> X (row-major, zeros left of the diagonal)
+template <int N, int B>
+__device__ __forceinline__ bool store_rows(double* __restrict__ dst, const double* xs, int r0, int rank, int nthr) {
+  bool finite = true;
+  constexpr int H = N / 2;  // 16-byte units per row
+  for (int u = rank; u < B * H; u += nthr) {
+    const int i = u / H, r = r0 + i, c = 2 * (u - i * H);
+    double2 v = make_double2(0.0, 0.0);
+    if (c >= 4 * (r >> 2)) {
+      v = *reinterpret_cast<const double2*>(xs + Rows<N>::at(r, c));
+      finite = finite && isfinite(v.x) && isfinite(v.y);
+    }
+    __stcs(reinterpret_cast<double2*>(dst + r * N + c), v);
+  }
+  return finite;
+}
+
+template <int N, int B>
+__global__ void __launch_bounds__(eng::WPolicy<0, N>::WARPS * 32, 1)
+    chol_rows_kernel(const double* __restrict__ A, double* __restrict__ X, int* __restrict__ info,
+                     long long batch) {
+  using P = eng::WPolicy<0, N>;
+  static_assert(P::SLOT == Rows<N>::DOUBLES, "packed rows and upper tiles have the same size");
+  constexpr int WG = P::WG, G = WG * 32, NB = N / B;
+  extern __shared__ double smem[];
+  int* gflag = reinterpret_cast<int*>(smem + (size_t)P::P * P::DB * P::SLOT);
+  int* gbad = gflag + 16;
+  double* rsb_all = reinterpret_cast<double*>(gbad + 16);
+  double* scr_all = rsb_all + P::P * P::RSB;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  Grp gr;
+  gr.id = warp / WG;
+  gr.wig = warp % WG;
+  gr.rank = threadIdx.x % G;
+  gr.rsb = rsb_all + P::RSB * gr.id;
+  gr.scr = P::SCR ? scr_all + (size_t)P::SCR * gr.id : nullptr;
+  gr.prof = nullptr;
+  // warps 1..WG-1 of group g: named barrier 1 + P + g (group barriers: 1 .. P)
+  const int subbar = (WG > 2 && 1 + P::P + gr.id <= 15) ? 1 + P::P + gr.id : 0;
+  if (!subbar) gr.scr = (WG > 2) ? nullptr : gr.scr;  // split-K needs the sub-group barrier
+  auto slot_at = [&](int d) { return smem + ((size_t)gr.id * P::DB + (d % P::DB)) * P::SLOT; };
+  constexpr long long NN = (long long)N * N;
+  const long long stride = (long long)gridDim.x * P::P;
+  long long prob = (long long)blockIdx.x * P::P + gr.id;
+  if (prob < batch) {
+    load_rows<N, G>(slot_at(0), A + prob * NN, gr.rank);
+    cp_async_commit();
+  }
+  int cur = 0;
+  for (; prob < batch; prob += stride) {
+    const long long off = prob * NN;
+    const long long nxt = prob + stride;
+    double* xs = slot_at(cur);
+    if constexpr (P::DB == 2) {
+      if (nxt < batch) {
+        load_rows<N, G>(slot_at(cur ^ 1), A + nxt * NN, gr.rank);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+    } else {
+      cp_async_wait<0>();
+    }
+    if (gr.rank == 0) {
+      gflag[gr.id] = 0;
+      gbad[gr.id] = 0;
+    }
+    gsync<WG>(gr);
+    int flag = 0;
+    bool fin = true;
+#pragma unroll 1
+    for (int k = 0; k < NB; ++k) {
+      const int r0 = k * B;
+      if constexpr (WG == 1) {
+        if (r0 > 0) s1_tile<N, B>(xs, r0);
+        __syncwarp();
+        leaf<N, B>(xs, r0, gr.rsb, &flag);
+        s3<N, B, WG>(xs, r0, 0, 1, gr, 0, 32);
+        __syncwarp();
+      } else {
+        if (gr.wig == 0) {
+          if (r0 > 0) s1_tile<N, B>(xs, r0);
+          __syncwarp();
+          leaf<N, B>(xs, r0, gr.rsb, &flag);
+        } else if constexpr (WG == 2) {
+          s3<N, B, WG>(xs, r0, 0, 1, gr, 0, 32);
+        } else {
+          s3<N, B, WG>(xs, r0, gr.wig - 1, WG - 1, gr, subbar, 32 * (WG - 1));
+        }
+        gsync<WG>(gr);
+      }
+      trsm<N, B>(xs, r0, gr.rsb, gr.rank, G);
+      gsync<WG>(gr);
+      fin = store_rows<N, B>(X + off, xs, r0, gr.rank, G) && fin;
+    }
+    const bool allfin = __all_sync(0xffffffffu, fin);
+    if (gr.wig == 0 && lane == 0 && flag) gflag[gr.id] = flag;
+    if (lane == 0 && !allfin) atomicOr(&gbad[gr.id], 1);
+    gsync<WG>(gr);
+    if (info && gr.rank == 0) {
+      const int f = gflag[gr.id];
+      info[prob] = f ? f : (gbad[gr.id] ? -1 : 0);
+    }
+    if constexpr (P::DB == 1) {
+      gsync<WG>(gr);  // slot reads done before it is refilled
+      if (nxt < batch) {
+        load_rows<N, G>(slot_at(0), A + nxt * NN, gr.rank);
+        cp_async_commit();
+      }
+    } else {
+      cur ^= 1;
+    }
+  }
+}
+
+}  // namespace cr
+}  // namespace lagen

@@ -146,6 +146,7 @@ struct Grp {
   double* rsb;  // per-group: reciprocal pivots of the last CHOL leaf [0, 16) and
                 //            its factor, row-major B x B, at [16, 16 + B*B)
   double* scr;  // per-group split-K scratch ((WG - 1) * 256 doubles)
+  int subbar;   // named barrier of warps 1 .. WG-1 (0: none)
   unsigned long long* prof;  // cycle accounting buffer (profiling launches only)
 };
 // The warps / threads executing one statement: the whole group, or (when a
@@ -235,80 +236,139 @@ struct BStream {
 // ----------------------------------------------------------------------------
 // m <= 8 (block-row updates of the left-looking variants): 8 x 32 warp
 // blocks, one A fragment feeds four independent DMMA accumulators per k-step.
+// With fewer blocks than warps (late iterations: long k, few columns) the k
+// range is split across the warps and the partial accumulators are reduced
+// in fixed order through the group's scratch (deterministic).
 template <bool UP, class OV, class AV, class BV>
-__device__ __forceinline__ void gemm_row8(const OV& O, const AV& A, const BV& Bm, int m, int p, int q, double sgn,
-                                          const Sub& sb) {
+__device__ __forceinline__ void row8_block(const AV& A, const BV& Bm, int m, int q, int j0, int kb, int ke,
+                                           bool v[4], double c0[4], double c1[4]) {
+  const int lane = lane_id();
+  const int g = lane >> 2;
+  const int ra = (g < m) ? g : (g & 3);
+  int cb[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int jt = j0 + 8 * u;
+    v[u] = jt < q && !(UP && 0 >= jt + 8);
+    cb[u] = (jt + g < q) ? jt + g : (jt < q ? jt + (g & 3) : j0 + (g & 3));
+  }
+  AStream<AV> as;
+  BStream<BV> bs[4];
+  as.init(A, ra, kb);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) bs[u].init(Bm, cb[u], kb);
+  // two accumulator sets (even / odd k-steps): eight independent DMMA
+  // chains per warp hide the DMMA latency
+  double e0[4] = {0, 0, 0, 0}, e1[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) c0[u] = c1[u] = 0.0;
+  int k0 = kb;
+  for (; k0 + 8 <= ke; k0 += 8) {
+    const double a = as.load(A.base);
+    double bv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bv[u] = v[u] ? bs[u].load(Bm.base) : 0.0;
+    as.step();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bs[u].step();
+    const double a2 = as.load(A.base);
+    double bw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bw[u] = v[u] ? bs[u].load(Bm.base) : 0.0;
+    as.step();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bs[u].step();
+    // unconditional MMAs (invalid tiles multiply zeros): a predicated
+    // mma.sync costs a WARPSYNC per instruction
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(c0[u], c1[u], a, bv[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(e0[u], e1[u], a2, bw[u]);
+  }
+  if (k0 < ke) {
+    const double a = as.load(A.base);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dmma(c0[u], c1[u], a, v[u] ? bs[u].load(Bm.base) : 0.0);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    c0[u] += e0[u];
+    c1[u] += e1[u];
+  }
+}
+
+template <bool UP, class OV>
+__device__ __forceinline__ void row8_write(const OV& O, int m, int q, int j0, double sgn, const bool v[4],
+                                           const double c0[4], const double c1[4]) {
   const int lane = lane_id();
   const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (!v[u]) continue;
+    const int i = g, j = j0 + 8 * u + 2 * t;
+    if (i < m && j < q && (!UP || i <= j)) {
+      double& o0 = O.ref(i, j);
+      o0 = fma(sgn, c0[u], o0);
+    }
+    if (i < m && j + 1 < q && (!UP || i <= j + 1)) {
+      double& o1 = O.ref(i, j + 1);
+      o1 = fma(sgn, c1[u], o1);
+    }
+  }
+}
+
+template <bool UP, int WG, class OV, class AV, class BV>
+__device__ __forceinline__ void gemm_row8(const OV& O, const AV& A, const BV& Bm, int m, int p, int q, double sgn,
+                                          const Grp& gr, const Sub& sb) {
   const int nblk = (q + 31) >> 5;
-  const int ra = (g < m) ? g : (g & 3);
-  for (int bk = sb.w; bk < nblk; bk += sb.nw) {
-    const int j0 = bk << 5;
-    bool v[4];
-    int cb[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int jt = j0 + 8 * u;
-      v[u] = jt < q && !(UP && 0 >= jt + 8);
-      cb[u] = (jt + g < q) ? jt + g : (jt < q ? jt + (g & 3) : j0 + (g & 3));
+  // k-split factor: idle warps take slices of k (needs scratch and a barrier
+  // covering exactly the executing warps)
+  const bool can_split = WG > 1 && gr.scr != nullptr && (sb.full || gr.subbar != 0);
+  const int ks = (can_split && nblk < sb.nw) ? min(sb.nw / nblk, p / 16) : 1;
+  if (ks <= 1) {
+    for (int bk = sb.w; bk < nblk; bk += sb.nw) {
+      bool v[4];
+      double c0[4], c1[4];
+      row8_block<UP, OV>(A, Bm, m, q, bk << 5, 0, p, v, c0, c1);
+      row8_write<UP>(O, m, q, bk << 5, sgn, v, c0, c1);
     }
-    AStream<AV> as;
-    BStream<BV> bs[4];
-    as.init(A, ra, 0);
+    return;
+  }
+  auto bar = [&]() {
+    if (sb.full) gsync<WG>(gr);
+    else asm volatile("bar.sync %0, %1;" ::"r"(gr.subbar), "r"(sb.nthr) : "memory");
+  };
+  const int item = sb.w, blk = item % nblk, sl = item / nblk;  // slice sl of block blk
+  const bool active = item < nblk * ks;
+  bool v[4];
+  double c0[4], c1[4];
+  const int lane = lane_id();
+  if (active) {
+    const int ksteps = p >> 2;
+    const int kb = 4 * ((ksteps * sl) / ks), ke = 4 * ((ksteps * (sl + 1)) / ks);
+    row8_block<UP, OV>(A, Bm, m, q, blk << 5, kb, ke, v, c0, c1);
+    if (sl > 0) {
+      double* sp = gr.scr + ((sl - 1) * nblk + blk) * 256 + lane * 8;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) bs[u].init(Bm, cb[u], 0);
-    // two accumulator sets (even / odd k-steps): eight independent DMMA
-    // chains per warp hide the DMMA latency
-    double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
-    double e0[4] = {0, 0, 0, 0}, e1[4] = {0, 0, 0, 0};
-    int k0 = 0;
-    for (; k0 + 8 <= p; k0 += 8) {
-      const double a = as.load(A.base);
-      double bv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) bv[u] = v[u] ? bs[u].load(Bm.base) : 0.0;
-      as.step();
-#pragma unroll
-      for (int u = 0; u < 4; ++u) bs[u].step();
-      const double a2 = as.load(A.base);
-      double bw[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) bw[u] = v[u] ? bs[u].load(Bm.base) : 0.0;
-      as.step();
-#pragma unroll
-      for (int u = 0; u < 4; ++u) bs[u].step();
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (v[u]) dmma(c0[u], c1[u], a, bv[u]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (v[u]) dmma(e0[u], e1[u], a2, bw[u]);
-    }
-    if (k0 < p) {
-      const double a = as.load(A.base);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (v[u]) dmma(c0[u], c1[u], a, bs[u].load(Bm.base));
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      c0[u] += e0[u];
-      c1[u] += e1[u];
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (!v[u]) continue;
-      const int i = g, j = j0 + 8 * u + 2 * t;
-      if (i < m && j < q && (!UP || i <= j)) {
-        double& o0 = O.ref(i, j);
-        o0 = fma(sgn, c0[u], o0);
-      }
-      if (i < m && j + 1 < q && (!UP || i <= j + 1)) {
-        double& o1 = O.ref(i, j + 1);
-        o1 = fma(sgn, c1[u], o1);
+      for (int u = 0; u < 4; ++u) {
+        sp[2 * u] = c0[u];
+        sp[2 * u + 1] = c1[u];
       }
     }
   }
+  bar();
+  if (active && sl == 0) {
+    for (int s2 = 1; s2 < ks; ++s2) {
+      const double* sp = gr.scr + ((s2 - 1) * nblk + blk) * 256 + lane * 8;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c0[u] += sp[2 * u];
+        c1[u] += sp[2 * u + 1];
+      }
+    }
+    row8_write<UP>(O, m, q, blk << 5, sgn, v, c0, c1);
+  }
+  bar();  // scratch free for the next split GEMM of this (sub-)group
 }
 
 // single 8x8 output tile (m, q <= 8) on one warp: four independent
@@ -364,7 +424,7 @@ __device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int
     return;
   }
   if (m <= 8 && q > 8) {
-    gemm_row8<UP>(O, A, Bm, m, p, q, sgn, sb);
+    gemm_row8<UP, WG>(O, A, Bm, m, p, q, sgn, gr, sb);
     return;
   }
   const int lane = lane_id();
@@ -402,10 +462,12 @@ __device__ __forceinline__ void gemm(const OV& O, const AV& A, const BV& Bm, int
         const double b0 = b0s.load(Bm.base);
         const double a1 = a1s.load(A.base);
         const double b1 = b1s.load(Bm.base);
-        if (v00) dmma(c00a, c00b, a0, b0);
-        if (v01) dmma(c01a, c01b, a0, b1);
-        if (v10) dmma(c10a, c10b, a1, b0);
-        if (v11) dmma(c11a, c11b, a1, b1);
+        // unconditional (clamped operands are finite; invalid tiles are
+        // discarded at write-back): no WARPSYNC per predicated mma.sync
+        dmma(c00a, c00b, a0, b0);
+        dmma(c01a, c01b, a0, b1);
+        dmma(c10a, c10b, a1, b0);
+        dmma(c11a, c11b, a1, b1);
         a0s.step();
         a1s.step();
         b0s.step();
@@ -1215,7 +1277,10 @@ __device__ __forceinline__ void exec_if(const Slot& s, const Rep<N, B>& rp, int*
       sb.nthr = 32 * WG;
       sb.full = true;
     }
+    const long long t0 = gr.prof ? clock64() : 0;
     exec<EQ, N, B, WG, S>(s, rp, flag, gr, sb);
+    // per statement, per warp (warp 0 -> [12 + I], warp 1 -> [22 + I])
+    if (gr.prof && I < 10) gr.prof[(gr.wig == 0 ? 12 : 22) + I] += clock64() - t0;
   }
 }
 
@@ -1229,7 +1294,7 @@ __device__ __forceinline__ void run_level(const Slot& s, const Rep<N, B>& rp, in
   const long long t0 = clock64();
   (exec_if<EQ, N, B, WG, L, INFO, S, (int)I>(s, rp, flag, gr), ...);
   gsync<WG>(gr);
-  if (gr.prof) gr.prof[4 + L] += clock64() - t0;
+  if (gr.prof && gr.wig == 0) gr.prof[4 + L] += clock64() - t0;
 }
 
 template <int EQ, int N, int B, int WG, class INFO, class... S, int... Ls>
@@ -1243,7 +1308,11 @@ __device__ __forceinline__ void run_iter(const Slot& s, const Rep<N, B>& rp, int
 // the iteration, overlapping the output writes with later iterations.
 template <class... S>
 struct RowFinal {
+#ifdef LAGEN_NO_ROW_STREAM
+  static constexpr bool value = false;
+#else
   static constexpr bool value = ((S::out::r == 1 && S::out::c == 2) || ...);
+#endif
 };
 
 template <int N, class M, int G>
@@ -1446,7 +1515,9 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
   gr.rank = threadIdx.x % G;
   gr.rsb = rsb_all + P::RSB * gr.id;
   gr.scr = P::SCR ? scr_all + (size_t)P::SCR * gr.id : nullptr;
-  gr.prof = (prof && blockIdx.x == 0 && gr.id == 0 && gr.rank == 0) ? prof : nullptr;
+  gr.prof = (prof && blockIdx.x == 0 && gr.id == 0 && (gr.rank == 0 || gr.rank == 32)) ? prof : nullptr;
+  // warps 1 .. WG-1 of group g synchronise on barrier 1 + P + g (group barriers use 1 .. P)
+  gr.subbar = (WG > 2 && 1 + P::P + gr.id <= 15) ? 1 + P::P + gr.id : 0;
   auto slot_at = [&](int d) {
     Slot sl;
     double* base = smem + ((size_t)gr.id * P::DB + (d % P::DB)) * P::SLOT;
@@ -1486,10 +1557,10 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
     }
     int flag = 0;
     const long long tw1 = clock64();
-    if (gr.prof) gr.prof[0] += tw1 - tw0;  // wait for this problem's tiles
+    if (gr.prof && gr.wig == 0) gr.prof[0] += tw1 - tw0;  // wait for this problem's tiles
     bool fin = run_variant<EQ, N, B, WG>(VAR{}, s, &flag, gr, X + off);
     const long long tw2 = clock64();
-    if (gr.prof) {
+    if (gr.prof && gr.wig == 0) {
       gr.prof[1] += tw2 - tw1;  // compute
       gr.prof[3] += 1;          // problems
     }
@@ -1503,7 +1574,7 @@ __global__ void __launch_bounds__(WPolicy<EQ, N>::WARPS * 32, 1)
       const int f = gflag[gr.id];
       info[prob] = f ? f : (gbad[gr.id] ? -1 : 0);
     }
-    if (gr.prof) gr.prof[2] += clock64() - tw2;  // store + guards
+    if (gr.prof && gr.wig == 0) gr.prof[2] += clock64() - tw2;  // store + guards
     if constexpr (P::DB == 1) {
       gsync<WG>(gr);  // slot reads done before it is refilled
       if (nxt < batch) issue_loads<EQ, N, G>(slot_at(0), in0, in1, in2, nxt * NN, gr.rank);

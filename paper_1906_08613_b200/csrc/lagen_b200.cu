@@ -12,6 +12,8 @@
 #include "lagen_b200.h"
 #include "registry.cuh"
 #include "registry_col.cuh"
+#include "registry_df.cuh"
+#include "registry_rows.cuh"
 #include "registry_warp.cuh"
 #include "variants_table.h"
 
@@ -44,6 +46,26 @@ const ColEntry* find_col(int eq, int n, int b, int variant) {
   if (eq != 0 || variant < 0) return nullptr;
   for (int p = 0; p < kColParts; ++p) {
     const ColTable& t = kColTables[p];
+    for (int i = 0; i < *t.n; ++i)
+      if (t.e[i].n == n && t.e[i].b == b && t.e[i].variant == variant) return &t.e[i];
+  }
+  return nullptr;
+}
+
+const DfEntry* find_df(int eq, int n, int b, int variant) {
+  if (eq < 0 || eq > 2 || variant < 0) return nullptr;
+  for (int p = 0; p < kDfParts; ++p) {
+    const DfTable& t = kDfTables[p];
+    for (int i = 0; i < *t.n; ++i)
+      if (t.e[i].eq == eq && t.e[i].n == n && t.e[i].b == b && t.e[i].variant == variant) return &t.e[i];
+  }
+  return nullptr;
+}
+
+const RowsEntry* find_rows(int eq, int n, int b, int variant) {
+  if (eq != 0 || variant < 0) return nullptr;
+  for (int p = 0; p < kRowsParts; ++p) {
+    const RowsTable& t = kRowsTables[p];
     for (int i = 0; i < *t.n; ++i)
       if (t.e[i].n == n && t.e[i].b == b && t.e[i].variant == variant) return &t.e[i];
   }
@@ -210,6 +232,8 @@ int lagen_b200_engine_supported(int eq, int n, int b, int variant, int engine) {
     case LAGEN_ENGINE_GENERIC: return find_entry(eq, n, b) ? 1 : 0;
     case LAGEN_ENGINE_WARP: return find_warp(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_COLUMN: return find_col(eq, n, b, variant) ? 1 : 0;
+    case LAGEN_ENGINE_DATAFLOW: return find_df(eq, n, b, variant) ? 1 : 0;
+    case LAGEN_ENGINE_ROWS: return find_rows(eq, n, b, variant) ? 1 : 0;
   }
   return 0;
 }
@@ -227,7 +251,7 @@ int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n
 int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                const double* const* inputs, double* X, int* info, void* stream, int engine,
                                unsigned long long* d_prof) {
-  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_COLUMN) return fail(LAGEN_EINVAL, "unknown engine");
+  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWS) return fail(LAGEN_EINVAL, "unknown engine");
   int rc = check_common(eq, n, b, batch);
   if (rc) return rc;
   rc = validate(eq, stmts, nstmts);
@@ -254,7 +278,15 @@ int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int 
       return fail(LAGEN_EUNSUPPORTED, "no column-engine instance for this (variant, n, b)");
     if (engine == LAGEN_ENGINE_WARP && !w)
       return fail(LAGEN_EUNSUPPORTED, "no warp-engine instance for this (variant, n, b)");
-    if (c) fn = c->launch;
+    const DfEntry* d = (engine == LAGEN_ENGINE_DATAFLOW) ? find_df(eq, n, b, v) : nullptr;
+    if (engine == LAGEN_ENGINE_DATAFLOW && !d)
+      return fail(LAGEN_EUNSUPPORTED, "no dataflow-engine instance for this (variant, n, b)");
+    const RowsEntry* st = (engine == LAGEN_ENGINE_ROWS) ? find_rows(eq, n, b, v) : nullptr;
+    if (engine == LAGEN_ENGINE_ROWS && !st)
+      return fail(LAGEN_EUNSUPPORTED, "no rows-engine instance for this (variant, n, b)");
+    if (st) fn = st->launch;
+    else if (d) fn = d->launch;
+    else if (c) fn = c->launch;
     else if (w) fn = w->launch;
   }
   cudaError_t err = fn(a, static_cast<cudaStream_t>(stream));

@@ -57,7 +57,7 @@ def test_golden_reference_vectors(eq):
         groups.setdefault((e["n"], e["variant"], e["b"]), []).append(e)
     from paper_1906_08613_b200 import _lib
     for (n, v, b), es in groups.items():
-      for engine in ("generic", "warp", "column"):
+      for engine in ("generic", "warp", "column", "dataflow", "rows"):
         if not _lib.engine_supported(EQ_CODES[eq], n, b, v, engine):
             continue
         ins = [np.stack([d[f"in_{e['case']}_{n}_{nm}"] for e in es]) for nm in EQ_INPUTS[eq]]
@@ -89,7 +89,7 @@ def test_every_variant_vs_oracle(eq, n, oracle_mod):
     assert (ref_info == 0).all()
     res_tol = 10 * n * EPS
     from paper_1906_08613_b200 import _lib
-    runs = [(v, b, e) for e in ("generic", "warp", "column") for v in vs for b in default_blocks(n)
+    runs = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows") for v in vs for b in default_blocks(n)
             if _lib.engine_supported(EQ_CODES[eq], n, b, v.index, e)]
     for v, b, engine in runs:
         if True:
@@ -123,18 +123,27 @@ def test_known_answers():
 
 
 def test_non_spd_and_nan_are_reported():
-    n = 16
-    A = executor.generate("cholesky", n, seed=1, batch=4)[0]
-    A[2, 6, 6] = -1000.0
-    with pytest.raises(errors.VerificationError):
-        executor.solve("cholesky", [A], variant=2, b=4)
-    X, info = executor.solve("cholesky", [A], variant=2, b=4, check=False)
-    info = info.cpu().numpy()
-    assert info[2] == 7 and info[0] == 0 and info[1] == 0 and info[3] == 0
-    L, U, C = executor.generate("sylvester", n, seed=1, batch=3)
-    C[1, 0, 0] = float("nan")
-    _, info = executor.solve("sylvester", [L, U, C], variant=13, b=4, check=False)
-    assert info.cpu().tolist() == [0, -1, 0]
+    """info = first non-positive pivot + 1 (kernels.py:87-88) / -1 for NaN-Inf,
+    on every engine that has the variant."""
+    from paper_1906_08613_b200 import _lib
+    for n, bad in ((16, 6), (48, 37)):
+        A = executor.generate("cholesky", n, seed=1, batch=4)[0]
+        A[2, bad, bad] = -1000.0
+        with pytest.raises(errors.VerificationError):
+            executor.solve("cholesky", [A], variant=2, b=4)
+        for v in (1, 2):
+            for engine in ("generic", "warp", "column", "dataflow", "rows"):
+                if not _lib.engine_supported(0, n, 4, v, engine):
+                    continue
+                X, info = executor.solve("cholesky", [A], variant=v, b=4, check=False, engine=engine)
+                assert info.cpu().tolist() == [0, 0, bad + 1, 0], (n, v, engine)
+        L, U, C = executor.generate("sylvester", n, seed=1, batch=3)
+        C[1, 0, 0] = float("nan")
+        for engine in ("generic", "warp", "dataflow"):
+            if not _lib.engine_supported(2, n, 4, 13, engine):
+                continue
+            _, info = executor.solve("sylvester", [L, U, C], variant=13, b=4, check=False, engine=engine)
+            assert info.cpu().tolist() == [0, -1, 0], (n, engine)
     try:
         import lagen.errors
         with pytest.raises(lagen.errors.VerificationError):

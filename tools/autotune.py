@@ -55,7 +55,7 @@ def main():
             rows = []
             ref_X = None
             from paper_1906_08613_b200 import _lib
-            cands = [(v, b, e) for e in ("generic", "warp", "column")
+            cands = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows")
                      for v in builtin_variants(eq) for b in default_blocks(n)
                      if _lib.engine_supported(_lib_eq(eq), n, b, v.index, e)]
             if args.engines != "all":

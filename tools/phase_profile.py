@@ -34,3 +34,5 @@ nprob = max(1, p[3])
 print(f"{a.eq} n={a.n} v{a.variant} b{a.b}: problems={p[3]} cycles/problem: wait={p[0]/nprob:.0f} "
       f"compute={p[1]/nprob:.0f} store={p[2]/nprob:.0f}  levels=" +
       " ".join(f"L{i}:{p[4+i]/nprob:.0f}" for i in range(8) if p[4 + i]))
+for i, stmt in enumerate(st[:10]):
+    print(f"  s{i} {stmt['kind']}->{tuple(stmt['out'])}: warp0 {p[12+i]/nprob:.0f}  warp1 {p[22+i]/nprob:.0f}")
