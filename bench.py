@@ -257,7 +257,7 @@ def run_sweep(eq, cases, rank, steps, warmup, peaks, flush_l2=False, per_n_reps=
             t_roof_nom = batch * max(f_alg / (NOMINAL_FP64_TFLOPS * 1e12), byt / (NOMINAL_HBM_GBS * 1e9))
             t_roof_meas = batch * max(f_alg / (peaks["fp64_tflops"] * 1e12), byt / (peaks["hbm_gbs"] * 1e9))
             per_n.append({
-                "n": n, "batch": batch, "variant": p.variant, "b": p.b, "ms": round(ms, 5),
+                "n": n, "batch": batch, "variant": p.variant, "b": p.b, "engine": p.engine, "ms": round(ms, 5),
                 "gflops": round(batch * f_nom / t / 1e9, 1),
                 "gflops_alg": round(batch * f_alg / t / 1e9, 1),
                 "gbs": round(batch * byt / t / 1e9, 1),
@@ -295,13 +295,13 @@ def run_e2e(eq, plans, steps, world):
     d2h = sum(out.numel() * 8 + info.numel() * 4 for _, _, out, info in hosts)
     # warm-up one pass
     for p, ins, out, info in hosts:
-        executor.solve_host(eq, ins, variant=p.variant, b=p.b, out=out, info=info)
+        executor.solve_host(eq, ins, variant=p.variant, b=p.b, out=out, info=info, engine=p.engine)
     torch.cuda.synchronize()
     barrier(world)
     t0 = time.perf_counter()
     for _ in range(steps):
         for p, ins, out, info in hosts:
-            executor.solve_host(eq, ins, variant=p.variant, b=p.b, out=out, info=info)
+            executor.solve_host(eq, ins, variant=p.variant, b=p.b, out=out, info=info, engine=p.engine)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     barrier(world)
@@ -463,7 +463,7 @@ def main():
         line["e2e"] = {"value": round(sum_over_ranks(res["flops_nominal"], world) / dt / 1e9, 2),
                        "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                        "steps": e2e_steps,
-                       "path": "executor.solve_host -> lagen_b200_execute_host (pinned host buffers, "
+                       "path": "executor.solve_host -> lagen_b200_execute_host_engine (pinned host buffers, "
                                "chunked H2D/solve/D2H over two streams)"}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(eq, cases, budget_s=args.cpu_budget,

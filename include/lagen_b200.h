@@ -110,9 +110,11 @@ int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b
                        int* info, void* stream);
 
 /* Engine selection: LAGEN_ENGINE_AUTO picks, for a statement
- * list equal to a built-in variant, the register-resident "column engine"
- * (Cholesky, n <= 64) or the compiled-in "warp engine" when they have an
- * instance for (n, b); otherwise the generic statement-list kernel. */
+ * list equal to a built-in variant, the "rows engine" (Cholesky v1, n > 32),
+ * the register-resident "column engine" (Cholesky v1/v2, n <= 64) or the
+ * compiled-in "warp engine" when they have an instance for (n, b); otherwise
+ * the generic statement-list kernel.  The Python layer passes the engine of
+ * the GPU-measured dispatch table explicitly. */
 #define LAGEN_ENGINE_AUTO 0
 #define LAGEN_ENGINE_GENERIC 1
 #define LAGEN_ENGINE_WARP 2
@@ -143,6 +145,11 @@ int lagen_b200_engine_supported(int eq, int n, int b, int variant, int engine);
 int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
                             long long batch, const double* const* h_inputs,
                             double* h_X, int* h_info);
+/* Same with an explicit engine (LAGEN_ENGINE_*), so the host path runs the
+ * kernel the device path's dispatch picked (bit-identical results). */
+int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
+                                   long long batch, const double* const* h_inputs,
+                                   double* h_X, int* h_info, int engine);
 
 /* ---- seeded batched generator (BASELINE.json configs) ----
  * Writes problems [first, first + batch) of the seeded stream into outputs[]

@@ -44,6 +44,7 @@ def _load():
     lib.lagen_b200_execute_profile.argtypes = [i, vp, i, i, i, ll, vp, vp, vp, vp, i, vp]
     lib.lagen_b200_engine_supported.argtypes = [i, i, i, i, i]
     lib.lagen_b200_execute_host.argtypes = [i, vp, i, i, i, ll, vp, vp, vp]
+    lib.lagen_b200_execute_host_engine.argtypes = [i, vp, i, i, i, ll, vp, vp, vp, i]
     lib.lagen_b200_generate.argtypes = [i, i, ctypes.c_ulonglong, ll, ll, vp, vp]
     lib.lagen_b200_cholesky.argtypes = [i, i, i, ll, vp, vp, vp, vp]
     lib.lagen_b200_lyapunov.argtypes = [i, i, i, ll, vp, vp, vp, vp, vp]
@@ -58,7 +59,7 @@ EXPORTED = (
     "lagen_b200_abi_version", "lagen_b200_last_error", "lagen_b200_num_variants",
     "lagen_b200_variant_stmts", "lagen_b200_supported", "lagen_b200_geometry",
     "lagen_b200_cholesky", "lagen_b200_lyapunov", "lagen_b200_sylvester",
-    "lagen_b200_execute", "lagen_b200_execute_host", "lagen_b200_generate",
+    "lagen_b200_execute", "lagen_b200_execute_host", "lagen_b200_execute_host_engine", "lagen_b200_generate",
     "lagen_b200_execute_engine", "lagen_b200_warp_supported", "lagen_b200_engine_supported",
     "lagen_b200_execute_profile",
 )

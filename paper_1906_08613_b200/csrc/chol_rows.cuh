@@ -63,51 +63,49 @@ struct KRow {
   }
 };
 
-// row-major n x n (upper part) -> packed rows, cp.async 16-byte units
+// row-major n x n (upper part) -> packed rows, cp.async 16-byte units; full
+// rows are walked (division by the compile-time half-width) and the chunks
+// left of each row's first stored column are skipped
 template <int N, int G>
 __device__ __forceinline__ void load_rows(double* xs, const double* __restrict__ src, int rank) {
-#pragma unroll 1
-  for (int R = 0; R < N / 4; ++R) {
-    const int per = (N - 4 * R) >> 1;  // units per row of group R
-    for (int u = rank; u < 4 * per; u += G) {
-      const int r = 4 * R + u / per, c = 4 * R + 2 * (u % per);
-      cp_async16(xs + Rows<N>::at(r, c), src + r * N + c);
-    }
+  constexpr int H = N / 2;
+  for (int u = rank; u < N * H; u += G) {
+    const int r = u / H, c = 2 * (u - r * H);
+    if (c >= 4 * (r >> 2)) cp_async16(xs + Rows<N>::at(r, c), src + r * N + c);
   }
 }
 
-// S1: X11 (B x B upper) -= X01^T X01, K = r0; one warp, 4 accumulator chains
+// S1 part: X(t0:t0+B, t0:t0+B) (upper) -= sum over rows kk in [4 ks0, 4 ks1)
+// of X[kk][t0..]^T X[kk][t0..]; one warp, 4 accumulator chains
 template <int N, int B>
-__device__ __forceinline__ void s1_tile(double* xs, int r0) {
+__device__ __forceinline__ void s1_tile(double* xs, int t0, int ks0, int ks1) {
   const int lane = lane_id();
   const int g = lane >> 2, t = lane & 3;
   const int ga = (B == 8 || g < B) ? g : (g & 3);
   double c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
   KRow<N> kr;
-  kr.init(t, 0);
-  const int nks = r0 >> 2;
-  int ks = 0;
-  for (; ks + 4 <= nks; ks += 4) {
-    double a[4], b[4];
+  kr.init(t, ks0);
+  int ks = ks0;
+  for (; ks + 4 <= ks1; ks += 4) {
+    double a[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      a[u] = xs[kr.p + r0 + ga];
-      b[u] = xs[kr.p + r0 + (g & (B - 1))];
+      a[u] = xs[kr.p + t0 + ga];
       kr.step();
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) dmma(c0[u], c1[u], a[u], b[u]);
+    for (int u = 0; u < 4; ++u) dmma(c0[u], c1[u], a[u], a[u]);
   }
-  for (int u = 0; ks < nks; ++ks, ++u) {
-    const double a = xs[kr.p + r0 + ga], b = xs[kr.p + r0 + (g & (B - 1))];
+  for (int u = 0; ks < ks1; ++ks, ++u) {
+    const double a = xs[kr.p + t0 + ga];
     kr.step();
-    dmma(c0[u & 3], c1[u & 3], a, b);
+    dmma(c0[u & 3], c1[u & 3], a, a);
   }
   const double x0 = (c0[0] + c0[1]) + (c0[2] + c0[3]);
   const double x1 = (c1[0] + c1[1]) + (c1[2] + c1[3]);
   const int i = g, j = 2 * t;
   if (i < B && j < B) {
-    const int o = Rows<N>::at(r0 + i, r0 + j);
+    const int o = Rows<N>::at(t0 + i, t0 + j);
     if (i <= j) xs[o] -= x0;
     if (i <= j + 1 && j + 1 < B) xs[o + 1] -= x1;
   }
@@ -185,12 +183,14 @@ __device__ __forceinline__ void s3_write(double* xs, int r0, int c0, int cend, c
 // S3 over warps [w0, w0 + nw) (wi = this warp's index in that set); k split
 // across idle warps, partials reduced in fixed order through scratch.
 template <int N, int B, int WG>
-__device__ __forceinline__ void s3(double* xs, int r0, int wi, int nw, const Grp& gr, int bar_id, int bar_thr) {
+__device__ __forceinline__ void s3(double* xs, int r0, int wi, int nw, const Grp& gr, int bar_id, int bar_thr,
+                                   int split_mode) {
   const int cs = r0 + B, cend = N;
   if (cs >= cend || r0 == 0) return;
   const int nblk = (cend - cs + 31) >> 5;
   const int nks = r0 >> 2;
-  const int ks = (gr.scr != nullptr && nblk < nw) ? min(nw / nblk, nks / 4) : 1;
+  int ks = (gr.scr != nullptr && nblk < nw) ? min(nw / nblk, nks / 4) : 1;
+  if (split_mode == 0 || (split_mode == 2 && nblk > 1)) ks = 1;
   if (ks <= 1) {
     for (int bk = wi; bk < nblk; bk += nw) {
       double a0[4], a1[4];
@@ -253,7 +253,7 @@ __device__ __forceinline__ void leaf(double* xs, int r0, double* rsb, int* flag)
     }
   }
   double rs[B];
-  bool bad = false;
+  bool bad = false, nonfinite = false;
   int badi = 0;
 #pragma unroll
   for (int i = 0; i < B; ++i) {
@@ -262,6 +262,7 @@ __device__ __forceinline__ void leaf(double* xs, int r0, double* rsb, int* flag)
       bad = true;
       badi = i;
     }
+    nonfinite = nonfinite || !isfinite(piv);
     rs[i] = rsqrt(piv);
     t[i][i] = piv * rs[i];
 #pragma unroll
@@ -271,7 +272,10 @@ __device__ __forceinline__ void leaf(double* xs, int r0, double* rsb, int* flag)
 #pragma unroll
       for (int c = r; c < B; ++c) t[r][c] = fma(-t[i][r], t[i][c], t[r][c]);
   }
-  if (lane == 0 && bad && *flag == 0) *flag = r0 + badi + 1;
+  // first non-positive pivot -> its index + 1 (kernels.py:87-88); a NaN or
+  // infinite pivot (which every NaN / Inf of X reaches: each upper entry
+  // enters its column's diagonal through S1's square) -> -1 (verify.py:301)
+  if (lane == 0 && *flag == 0) *flag = bad ? r0 + badi + 1 : (nonfinite ? -1 : 0);
   double row[B];
   double rsr = 0.0;
 #pragma unroll
@@ -319,32 +323,50 @@ __device__ __forceinline__ void trsm(double* xs, int r0, const double* rsb, int 
 
 // block row [r0, r0 + B) -> X (row-major, zeros left of the diagonal)
 template <int N, int B>
-__device__ __forceinline__ bool store_rows(double* __restrict__ dst, const double* xs, int r0, int rank, int nthr) {
-  bool finite = true;
+__device__ __forceinline__ void store_rows(double* __restrict__ dst, const double* xs, int r0, int rank, int nthr) {
   constexpr int H = N / 2;  // 16-byte units per row
   for (int u = rank; u < B * H; u += nthr) {
     const int i = u / H, r = r0 + i, c = 2 * (u - i * H);
     double2 v = make_double2(0.0, 0.0);
-    if (c >= 4 * (r >> 2)) {
-      v = *reinterpret_cast<const double2*>(xs + Rows<N>::at(r, c));
-      finite = finite && isfinite(v.x) && isfinite(v.y);
-    }
+    if (c >= 4 * (r >> 2)) v = *reinterpret_cast<const double2*>(xs + Rows<N>::at(r, c));
     __stcs(reinterpret_cast<double2*>(dst + r * N + c), v);
   }
-  return finite;
+}
+
+#ifdef LAGEN_ROWS_PROF
+__device__ unsigned long long prof_buf[16];
+#endif
+
+// Launch mode per size = k-split on (1) | work split << 2, measured with
+// LAGEN_ROWS_MODE=m tools/engine_compare.py over n = 36..128 (full 256 MiB
+// batches, profiles/r01_rows_modes.txt): look-ahead pays where warp 0's leaf
+// chain is the bottleneck, not where the 4x4 look-ahead tile overloads a warp.
+inline int default_mode(int n, int b) {
+  int ws = 3;
+  if (b == 4) {
+    if (n <= 44) ws = 1;
+    else if (n == 48 || n == 96 || n == 104 || n == 108 || n >= 120) ws = 3;
+    else if (n == 52 || n == 56 || n == 100 || n == 112 || n == 116) ws = 2;
+    else ws = 1;  // 60 .. 92
+  } else {
+    if (n == 40 || n == 56 || n == 112) ws = 0;
+    else if (n == 80 || n == 88) ws = 2;
+    else ws = 3;
+  }
+  return 1 | (ws << 2);
 }
 
 template <int N, int B>
 __global__ void __launch_bounds__(eng::WPolicy<0, N>::WARPS * 32, 1)
     chol_rows_kernel(const double* __restrict__ A, double* __restrict__ X, int* __restrict__ info,
-                     long long batch) {
+                     long long batch, int mode) {
+  const int split_mode = mode & 3, work_split = (mode >> 2) & 3;
   using P = eng::WPolicy<0, N>;
   static_assert(P::SLOT == Rows<N>::DOUBLES, "packed rows and upper tiles have the same size");
   constexpr int WG = P::WG, G = WG * 32, NB = N / B;
   extern __shared__ double smem[];
   int* gflag = reinterpret_cast<int*>(smem + (size_t)P::P * P::DB * P::SLOT);
-  int* gbad = gflag + 16;
-  double* rsb_all = reinterpret_cast<double*>(gbad + 16);
+  double* rsb_all = reinterpret_cast<double*>(gflag + 32);
   double* scr_all = rsb_all + P::P * P::RSB;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   Grp gr;
@@ -381,46 +403,73 @@ __global__ void __launch_bounds__(eng::WPolicy<0, N>::WARPS * 32, 1)
     } else {
       cp_async_wait<0>();
     }
-    if (gr.rank == 0) {
-      gflag[gr.id] = 0;
-      gbad[gr.id] = 0;
-    }
+    if (gr.rank == 0) gflag[gr.id] = 0;
     gsync<WG>(gr);
     int flag = 0;
-    bool fin = true;
+#ifdef LAGEN_ROWS_PROF
+    long long tp0 = clock64();
+    auto tick = [&](int slot) {
+      if (blockIdx.x == 0 && gr.id == 0 && lane == 0 && gr.wig < 2) {
+        const long long t1 = clock64();
+        atomicAdd(reinterpret_cast<unsigned long long*>(X) + 0, 0ull);  // keep ordering
+        prof_buf[gr.wig * 8 + slot] += t1 - tp0;
+        tp0 = t1;
+      }
+    };
+#else
+    auto tick = [](int) {};
+#endif
 #pragma unroll 1
     for (int k = 0; k < NB; ++k) {
       const int r0 = k * B;
       if constexpr (WG == 1) {
-        if (r0 > 0) s1_tile<N, B>(xs, r0);
+        if (r0 > 0) s1_tile<N, B>(xs, r0, 0, r0 >> 2);
         __syncwarp();
         leaf<N, B>(xs, r0, gr.rsb, &flag);
-        s3<N, B, WG>(xs, r0, 0, 1, gr, 0, 32);
+        s3<N, B, WG>(xs, r0, 0, 1, gr, 0, 32, split_mode);
         __syncwarp();
+        trsm<N, B>(xs, r0, gr.rsb, gr.rank, G);
+        __syncwarp();
+        store_rows<N, B>(X + off, xs, r0, gr.rank, G);
       } else {
+        // level A.  warp 0: the last block row's S1 contribution (K = B; the
+        // rows above were applied one iteration ahead), then the leaf.
+        // warps 1..WG-1: store block row k-1, S3 of this block row, and the
+        // look-ahead S1 part of block k+1 (all rows above r0 are final).
+        // who takes the store and the look-ahead beside warp 0's leaf chain
+        // (work split, tuned per size: default_mode()) — 0: warps 1..;
+        // 1: warp 0; 2: warp 0 stores, warps 1.. look ahead; 3: no look-ahead
+        // (warp 0 runs the whole S1), warps 1.. store
+        const bool ahead = work_split != 3;
+        const bool w0_store = work_split == 1 || work_split == 2, w0_look = work_split == 1;
         if (gr.wig == 0) {
-          if (r0 > 0) s1_tile<N, B>(xs, r0);
+          if (r0 > 0) s1_tile<N, B>(xs, r0, ahead ? (r0 - B) >> 2 : 0, r0 >> 2);
           __syncwarp();
           leaf<N, B>(xs, r0, gr.rsb, &flag);
-        } else if constexpr (WG == 2) {
-          s3<N, B, WG>(xs, r0, 0, 1, gr, 0, 32);
+          if (w0_store && r0 > 0) store_rows<N, B>(X + off, xs, r0 - B, lane, 32);
+          if (ahead && w0_look && r0 + B < N && r0 > 0) s1_tile<N, B>(xs, r0 + B, 0, r0 >> 2);
         } else {
-          s3<N, B, WG>(xs, r0, gr.wig - 1, WG - 1, gr, subbar, 32 * (WG - 1));
+          if (!w0_store && r0 > 0) store_rows<N, B>(X + off, xs, r0 - B, gr.rank - 32, 32 * (WG - 1));
+          if constexpr (WG == 2) {
+            s3<N, B, WG>(xs, r0, 0, 1, gr, 0, 32, split_mode);
+          } else {
+            s3<N, B, WG>(xs, r0, gr.wig - 1, WG - 1, gr, subbar, 32 * (WG - 1), split_mode);
+          }
+          if (ahead && !w0_look && r0 + B < N && r0 > 0 && gr.wig == WG - 1) s1_tile<N, B>(xs, r0 + B, 0, r0 >> 2);
         }
+        tick(0);
         gsync<WG>(gr);
+        tick(1);
+        trsm<N, B>(xs, r0, gr.rsb, gr.rank, G);
+        tick(2);
+        gsync<WG>(gr);
+        tick(3);
       }
-      trsm<N, B>(xs, r0, gr.rsb, gr.rank, G);
-      gsync<WG>(gr);
-      fin = store_rows<N, B>(X + off, xs, r0, gr.rank, G) && fin;
     }
-    const bool allfin = __all_sync(0xffffffffu, fin);
+    if constexpr (WG > 1) store_rows<N, B>(X + off, xs, N - B, gr.rank, G);
     if (gr.wig == 0 && lane == 0 && flag) gflag[gr.id] = flag;
-    if (lane == 0 && !allfin) atomicOr(&gbad[gr.id], 1);
     gsync<WG>(gr);
-    if (info && gr.rank == 0) {
-      const int f = gflag[gr.id];
-      info[prob] = f ? f : (gbad[gr.id] ? -1 : 0);
-    }
+    if (info && gr.rank == 0) info[prob] = gflag[gr.id];
     if constexpr (P::DB == 1) {
       gsync<WG>(gr);  // slot reads done before it is refilled
       if (nxt < batch) {

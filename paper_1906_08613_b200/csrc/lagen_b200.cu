@@ -281,7 +281,10 @@ int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int 
     const DfEntry* d = (engine == LAGEN_ENGINE_DATAFLOW) ? find_df(eq, n, b, v) : nullptr;
     if (engine == LAGEN_ENGINE_DATAFLOW && !d)
       return fail(LAGEN_EUNSUPPORTED, "no dataflow-engine instance for this (variant, n, b)");
-    const RowsEntry* st = (engine == LAGEN_ENGINE_ROWS) ? find_rows(eq, n, b, v) : nullptr;
+    // AUTO: the rows engine (Cholesky v1, n > 32) is the fastest measured path
+    // (dispatch_table.json); the register column engine below that
+    const RowsEntry* st =
+        (engine == LAGEN_ENGINE_ROWS || (engine == LAGEN_ENGINE_AUTO && n > 32)) ? find_rows(eq, n, b, v) : nullptr;
     if (engine == LAGEN_ENGINE_ROWS && !st)
       return fail(LAGEN_EUNSUPPORTED, "no rows-engine instance for this (variant, n, b)");
     if (st) fn = st->launch;
@@ -325,7 +328,13 @@ int lagen_b200_sylvester(int variant, int n, int b, long long batch, const doubl
 // busy (with 2 sets the H2D of chunk c+2 would wait for the D2H of chunk c).
 int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                             const double* const* h_inputs, double* h_X, int* h_info) {
+  return lagen_b200_execute_host_engine(eq, stmts, nstmts, n, b, batch, h_inputs, h_X, h_info, LAGEN_ENGINE_AUTO);
+}
+
+int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
+                                   const double* const* h_inputs, double* h_X, int* h_info, int engine) {
   constexpr int NS = 4;
+  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWS) return fail(LAGEN_EINVAL, "unknown engine");
   int rc = check_common(eq, n, b, batch);
   if (rc) return rc;
   rc = validate(eq, stmts, nstmts);
@@ -362,7 +371,7 @@ int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, 
       err = cudaMemcpyAsync(d_in[k][i], h_inputs[i] + c0 * n * n, cnt * prob_bytes, cudaMemcpyHostToDevice, st[k]);
     if (err != cudaSuccess) { status = cuda_fail(err, "H2D"); break; }
     const double* ins[3] = {d_in[k][0], d_in[k][1], d_in[k][2]};
-    status = lagen_b200_execute(eq, stmts, nstmts, n, b, cnt, ins, d_X[k], d_info[k], st[k]);
+    status = lagen_b200_execute_engine(eq, stmts, nstmts, n, b, cnt, ins, d_X[k], d_info[k], st[k], engine);
     if (status != LAGEN_OK) break;
     err = cudaMemcpyAsync(h_X + c0 * n * n, d_X[k], cnt * prob_bytes, cudaMemcpyDeviceToHost, st[k]);
     if (err == cudaSuccess && h_info)

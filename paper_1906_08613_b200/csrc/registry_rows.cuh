@@ -1,6 +1,7 @@
 // registry_rows.cuh — rows-engine instances (Cholesky v1, packed row-major X).
 #pragma once
 #include <atomic>
+#include <cstdlib>
 
 #include "chol_rows.cuh"
 #include "registry.cuh"
@@ -40,7 +41,13 @@ cudaError_t launch_rows(const LaunchArgs& a, cudaStream_t s) {
   const long long need = (a.batch + P::P - 1) / P::P;
   const long long resident = (long long)ctas_per_sm.load() * sm_count.load();
   const long long grid = need < resident ? need : resident;
-  kern<<<(unsigned)grid, P::WARPS * 32, P::SMEM, s>>>(a.in[0], a.X, a.info, a.batch);
+  // mode = k-split (bits 0-1) | work split (bits 2-3); LAGEN_ROWS_MODE
+  // overrides the tuned default (tuning runs only)
+  static const int mode = [] {
+    const char* e = std::getenv("LAGEN_ROWS_MODE");
+    return e ? std::atoi(e) : cr::default_mode(N, B);
+  }();
+  kern<<<(unsigned)grid, P::WARPS * 32, P::SMEM, s>>>(a.in[0], a.X, a.info, a.batch, mode);
   return cudaGetLastError();
 }
 

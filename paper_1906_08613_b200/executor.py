@@ -204,9 +204,10 @@ def interpret_algorithm(alg, inst, b, on_iteration=None):
     return {alg.output: X[0].cpu().numpy()}, flop_count(eq_name, stmts, n, b)
 
 
-def solve_host(eq, inputs, variant=None, b=None, out=None, info=None):
+def solve_host(eq, inputs, variant=None, b=None, out=None, info=None, engine=None):
     """Host buffers (numpy arrays or CPU tensors, ideally pinned) -> host X.
-    Streams the batch through the GPU with H2D / solve / D2H overlap."""
+    Streams the batch through the GPU with H2D / solve / D2H overlap; runs the
+    same kernel as solve() (dispatch-table engine unless given)."""
     eq_name = _eq_name(eq)
     arrs = []
     for t in inputs:
@@ -218,11 +219,17 @@ def solve_host(eq, inputs, variant=None, b=None, out=None, info=None):
             a = np.ascontiguousarray(t, dtype=np.float64)
             arrs.append(torch.from_numpy(a))
     batch, n = arrs[0].shape[0], arrs[0].shape[1]
-    stmts, _ = resolve_variant(eq_name, variant)
+    stmts, idx = resolve_variant(eq_name, variant)
     if stmts is None:
         pick = dispatch.select(eq_name, n)
         stmts = builtin_variants(eq_name)[pick["variant"]].statements
         b = b or pick["b"]
+        engine = engine or pick.get("engine")
+    elif b is None:
+        pick = dispatch.select(eq_name, n)
+        b = pick["b"]
+        if idx is not None and pick["variant"] == idx:
+            engine = engine or pick.get("engine")
     validate(eq_name, stmts)
     if out is None:
         out = torch.empty((batch, n, n), dtype=torch.float64, pin_memory=arrs[0].is_pinned())
@@ -230,9 +237,9 @@ def solve_host(eq, inputs, variant=None, b=None, out=None, info=None):
         info = torch.empty(batch, dtype=torch.int32)
     arr = _lib.stmt_array(stmts)
     ptrs = (ctypes.c_void_p * 3)(*([t.data_ptr() for t in arrs] + [0] * (3 - len(arrs))))
-    rc = _lib.lib.lagen_b200_execute_host(EQ_CODES[eq_name], ctypes.addressof(arr), len(stmts), n, b,
-                                          batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
-                                          ctypes.c_void_p(info.data_ptr()))
+    rc = _lib.lib.lagen_b200_execute_host_engine(EQ_CODES[eq_name], ctypes.addressof(arr), len(stmts), n, b,
+                                                 batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
+                                                 ctypes.c_void_p(info.data_ptr()), _lib.ENGINES[engine or "auto"])
     _lib.check(rc, f"{eq_name} host n={n} b={b}")
     return out, info
 
