@@ -36,6 +36,27 @@ using eng::Grp;
 using eng::gsync;
 using eng::lane_id;
 
+// Residency: WG warps own a problem (a template parameter; the launcher picks
+// it per size, rows_wg()), as many problems per CTA as shared memory allows,
+// double-buffered (next problem prefetched) when >= 6 still fit.
+template <int N, int WG_>
+struct RPolicy {
+  static constexpr int SLOT = N * N / 2 + 2 * N;
+  static constexpr int BUDGET = 220 * 1024;
+  static constexpr int WG = WG_;
+  static constexpr int S1 = BUDGET / (SLOT * 8 + 640);
+  static constexpr int S2 = BUDGET / (2 * SLOT * 8 + 640);
+  static constexpr int DB = S2 >= 6 ? 2 : 1;
+  static constexpr int P0 = DB == 2 ? S2 : (S1 < 1 ? 1 : S1);
+  static constexpr int PMAX = 32 / WG > 16 ? 16 : 32 / WG;  // <= 32 warps per CTA
+  static constexpr int P = P0 > PMAX ? PMAX : P0;
+  static constexpr int WARPS = P * WG;
+  static constexpr int RSB = 16 + 64;
+  static constexpr size_t BASE = (size_t)P * DB * SLOT * 8 + 2 * 16 * sizeof(int) + (size_t)P * RSB * 8;
+  static constexpr int SCR = (BASE + (size_t)P * (WG - 1) * 256 * 8 <= 227 * 1024) ? (WG - 1) * 256 : 0;
+  static constexpr size_t SMEM = BASE + (size_t)P * SCR * 8;
+};
+
 // packed upper rows: row r starts at column 4R (R = r / 4)
 template <int N>
 struct Rows {
@@ -337,31 +358,24 @@ __device__ __forceinline__ void store_rows(double* __restrict__ dst, const doubl
 __device__ unsigned long long prof_buf[16];
 #endif
 
-// Launch mode per size = k-split on (1) | work split << 2, measured with
-// LAGEN_ROWS_MODE=m tools/engine_compare.py over n = 36..128 (full 256 MiB
-// batches, profiles/r01_rows_modes.txt): look-ahead pays where warp 0's leaf
-// chain is the bottleneck, not where the 4x4 look-ahead tile overloads a warp.
-inline int default_mode(int n, int b) {
-  int ws = 3;
-  if (b == 4) {
-    if (n <= 44) ws = 1;
-    else if (n == 48 || n == 96 || n == 104 || n == 108 || n >= 120) ws = 3;
-    else if (n == 52 || n == 56 || n == 100 || n == 112 || n == 116) ws = 2;
-    else ws = 1;  // 60 .. 92
-  } else {
-    if (n == 40 || n == 56 || n == 112) ws = 0;
-    else if (n == 80 || n == 88) ws = 2;
-    else ws = 3;
-  }
-  return 1 | (ws << 2);
-}
+// Measured per size (index n / 4; b = 4 and b = 8): warps per problem and
+// launch mode = k-split (1) | work split << 2.  Sweep of WG in {1, 2, 4} x
+// modes {1, 5, 9, 13} over n = 36..128 at full 256 MiB batches
+// (LAGEN_ROWS_WG / LAGEN_ROWS_MODE + tools/engine_compare.py,
+// profiles/r01_rows_wg_modes.txt); sizes below 36 use the column engine.
+constexpr unsigned char kRowsWG[2][33] = {{1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 1, 1, 2, 1, 1, 2, 1, 2, 2, 2, 2, 2, 2, 2, 2, 2, 4, 4, 4},
+                                            {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 1, 2, 1, 1, 1, 1, 1, 2, 1, 2, 1, 2, 1, 2, 1, 4, 1, 4}};
+constexpr unsigned char kRowsMode[2][33] = {{1, 1, 1, 1, 1, 1, 1, 1, 1, 13, 1, 13, 13, 9, 5, 5, 13, 1, 13, 5, 1, 5, 5, 5, 5, 5, 5, 5, 5, 5, 13, 13, 13},
+                                              {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 5, 1, 5, 1, 13, 1, 13, 1, 9, 1, 1, 1, 9, 1, 9, 1, 9, 1, 9, 1, 13, 1, 13}};
+inline int rows_wg(int n, int b) { return kRowsWG[b == 8][n / 4]; }
+inline int default_mode(int n, int b) { return kRowsMode[b == 8][n / 4]; }
 
-template <int N, int B>
-__global__ void __launch_bounds__(eng::WPolicy<0, N>::WARPS * 32, 1)
+template <int N, int B, int WG_>
+__global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)
     chol_rows_kernel(const double* __restrict__ A, double* __restrict__ X, int* __restrict__ info,
                      long long batch, int mode) {
   const int split_mode = mode & 3, work_split = (mode >> 2) & 3;
-  using P = eng::WPolicy<0, N>;
+  using P = RPolicy<N, WG_>;
   static_assert(P::SLOT == Rows<N>::DOUBLES, "packed rows and upper tiles have the same size");
   constexpr int WG = P::WG, G = WG * 32, NB = N / B;
   extern __shared__ double smem[];
