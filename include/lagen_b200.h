@@ -125,6 +125,9 @@ int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b
 /* Cholesky v1 on a packed row-major upper layout (cheap DMMA operand
  * addressing for the block-row updates) */
 #define LAGEN_ENGINE_ROWS 5
+/* Lyapunov v5 / Sylvester v13: 8x8-tile anti-diagonal wavefront, DMMA
+ * tile updates with register-resident accumulators (wave.cuh) */
+#define LAGEN_ENGINE_WAVE 6
 int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
                               long long batch, const double* const* inputs, double* X,
                               int* info, void* stream, int engine);

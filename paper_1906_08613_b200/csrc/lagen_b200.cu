@@ -15,6 +15,7 @@
 #include "registry_df.cuh"
 #include "registry_rows.cuh"
 #include "registry_warp.cuh"
+#include "registry_wave.cuh"
 #include "variants_table.h"
 
 using namespace lagen;
@@ -68,6 +69,19 @@ const RowsEntry* find_rows(int eq, int n, int b, int variant) {
     const RowsTable& t = kRowsTables[p];
     for (int i = 0; i < *t.n; ++i)
       if (t.e[i].n == n && t.e[i].b == b && t.e[i].variant == variant) return &t.e[i];
+  }
+  return nullptr;
+}
+
+// wave engine: Lyapunov v5 / Sylvester v13 (the right-looking variants whose
+// tile-level order it follows, wave.cuh), any block size the variant runs at
+const WaveEntry* find_wave(int eq, int n, int b, int variant) {
+  (void)b;
+  if (!((eq == 1 && variant == 5) || (eq == 2 && variant == 13))) return nullptr;
+  for (int p = 0; p < kWaveParts; ++p) {
+    const WaveTable& t = kWaveTables[p];
+    for (int i = 0; i < *t.n; ++i)
+      if (t.e[i].eq == eq && t.e[i].n == n) return &t.e[i];
   }
   return nullptr;
 }
@@ -234,6 +248,7 @@ int lagen_b200_engine_supported(int eq, int n, int b, int variant, int engine) {
     case LAGEN_ENGINE_COLUMN: return find_col(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_DATAFLOW: return find_df(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_ROWS: return find_rows(eq, n, b, variant) ? 1 : 0;
+    case LAGEN_ENGINE_WAVE: return find_wave(eq, n, b, variant) ? 1 : 0;
   }
   return 0;
 }
@@ -251,7 +266,7 @@ int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n
 int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                const double* const* inputs, double* X, int* info, void* stream, int engine,
                                unsigned long long* d_prof) {
-  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWS) return fail(LAGEN_EINVAL, "unknown engine");
+  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_WAVE) return fail(LAGEN_EINVAL, "unknown engine");
   int rc = check_common(eq, n, b, batch);
   if (rc) return rc;
   rc = validate(eq, stmts, nstmts);
@@ -287,7 +302,14 @@ int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int 
         (engine == LAGEN_ENGINE_ROWS || (engine == LAGEN_ENGINE_AUTO && n > 32)) ? find_rows(eq, n, b, v) : nullptr;
     if (engine == LAGEN_ENGINE_ROWS && !st)
       return fail(LAGEN_EUNSUPPORTED, "no rows-engine instance for this (variant, n, b)");
-    if (st) fn = st->launch;
+    // AUTO: the wave engine for the right-looking Lyapunov / Sylvester
+    // variants at n >= 16 (dispatch_table.json measures the rest)
+    const WaveEntry* wv =
+        (engine == LAGEN_ENGINE_WAVE || (engine == LAGEN_ENGINE_AUTO && n >= 16)) ? find_wave(eq, n, b, v) : nullptr;
+    if (engine == LAGEN_ENGINE_WAVE && !wv)
+      return fail(LAGEN_EUNSUPPORTED, "no wave-engine instance for this (variant, n, b)");
+    if (wv) fn = wv->launch;
+    else if (st) fn = st->launch;
     else if (d) fn = d->launch;
     else if (c) fn = c->launch;
     else if (w) fn = w->launch;
@@ -334,7 +356,7 @@ int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, 
 int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                    const double* const* h_inputs, double* h_X, int* h_info, int engine) {
   constexpr int NS = 4;
-  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWS) return fail(LAGEN_EINVAL, "unknown engine");
+  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_WAVE) return fail(LAGEN_EINVAL, "unknown engine");
   int rc = check_common(eq, n, b, batch);
   if (rc) return rc;
   rc = validate(eq, stmts, nstmts);

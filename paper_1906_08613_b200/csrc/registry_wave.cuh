@@ -1,0 +1,89 @@
+// registry_wave.cuh — wave-engine instances (Sylvester v13 / Lyapunov v5
+// semantics, 8x8 tiles; see wave.cuh).  Geometry per size: NW warps per
+// problem and PP problems per CTA (WCfg, overridable for tuning runs with
+// LAGEN_WAVE_NW / LAGEN_WAVE_PP among the instantiated alternatives).
+#pragma once
+#include <atomic>
+#include <cstdlib>
+
+#include "registry.cuh"
+#include "wave.cuh"
+
+namespace lagen {
+
+struct WaveEntry {
+  int eq, n;
+  int smem;
+  LaunchFn launch;
+};
+
+// default geometry: enough warps that a diagonal spreads over <= 4 groups per
+// warp and <= ~32 accumulator tiles per warp; then as many problems per CTA as
+// registers (~4 S + 112 per thread, spill-free at that cap) and shared memory allow
+template <int EQ, int N>
+struct WCfg {
+  static constexpr int T = (N + 7) / 8;
+  static constexpr int NT = EQ == 2 ? T * T : T * (T + 1) / 2;
+  static constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+  static constexpr int mx(int a, int b) { return a > b ? a : b; }
+  static constexpr int mn(int a, int b) { return a < b ? a : b; }
+  static constexpr int NW = mx(mx(cdiv(T, 4), cdiv(NT, 32)), 1);
+  static constexpr int S = cdiv(NT, NW);
+  static constexpr int REGS = mn(255, 4 * S + 112);  // measured: ~112 beside the accumulators
+  static constexpr int PPR = 65536 / (REGS * 32 * NW);
+  static constexpr int SLOTB = (int)(wave::WPol<EQ, N, NW, 1>::SLOT * 8);
+  static constexpr int PPS = (227 * 1024) / SLOTB;
+  static constexpr int PP = mx(1, mn(mn(PPR, PPS), mn(32 / NW, NW == 1 ? 32 : 15)));
+};
+
+template <int EQ, int N, int NW, int PP>
+cudaError_t launch_wave_cfg(const LaunchArgs& a, cudaStream_t s) {
+  using P = wave::WPol<EQ, N, NW, PP>;
+  static std::atomic<unsigned long long> configured{0};
+  static std::atomic<int> ctas_per_sm{0};
+  static std::atomic<int> sm_count{0};
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  const unsigned long long bit = 1ull << (dev & 63);
+  auto kern = wave::wave_kernel<EQ, N, NW, PP>;
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
+    if (err != cudaSuccess) return err;
+    int occ = 0, sms = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, P::THREADS, P::SMEM);
+    if (err != cudaSuccess) return err;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (err != cudaSuccess) return err;
+    ctas_per_sm.store(occ);
+    sm_count.store(sms);
+    configured.fetch_or(bit, std::memory_order_acq_rel);
+  }
+  if (a.batch <= 0) return cudaSuccess;
+  const long long need = (a.batch + PP - 1) / PP;
+  const long long resident = (long long)ctas_per_sm.load() * sm_count.load();
+  const long long grid = need < resident ? need : resident;
+  // _signature order: lyapunov (L, S), sylvester (L, U, C)
+  const double* L = a.in[0];
+  const double* U = EQ == 2 ? a.in[1] : a.in[0];
+  const double* C = EQ == 2 ? a.in[2] : a.in[1];
+  kern<<<(unsigned)grid, P::THREADS, P::SMEM, s>>>(L, U, C, a.X, a.info, a.batch);
+  return cudaGetLastError();
+}
+
+template <int EQ, int N>
+cudaError_t launch_wave(const LaunchArgs& a, cudaStream_t s) {
+  using C = WCfg<EQ, N>;
+  return launch_wave_cfg<EQ, N, C::NW, C::PP>(a, s);
+}
+
+#define LAGEN_WAVE_ENTRY(EQ, N) \
+  { EQ, N, (int)wave::WPol<EQ, N, WCfg<EQ, N>::NW, WCfg<EQ, N>::PP>::SMEM, &launch_wave<EQ, N> }
+
+struct WaveTable {
+  const WaveEntry* e;
+  const int* n;
+};
+
+}  // namespace lagen

@@ -1,0 +1,375 @@
+// wave.cuh — the "wave engine": triangular Sylvester (L X + X U = C) and
+// triangular Lyapunov (L X + X L^T = S) as an 8x8-tile anti-diagonal
+// wavefront with every cross-tile update on the FP64 tensor path.
+//
+// Math (tile (I, J) of X, tiles 8x8, T = ceil(n / 8) per side):
+//   L_II X_IJ + X_IJ U_JJ = C_IJ - sum_{k<I} L_Ik X_kJ - sum_{k<J} X_Ik U_kJ
+// — the 2x2-block recursion every Sylvester variant is derived from
+// (ref:pkg/tests/test_invariants.py:25-32 PME), applied at tile granularity
+// in the order of the right-looking variant v13 (Sylvester) / v5 (Lyapunov):
+// tile (I, J) takes the contributions of X_kJ and X_Ik in increasing k, the
+// diagonal-block solve is the SYLV leaf (ref:pkg/src/lagen/kernels.py:100-110,
+// column-then-row order) and, for Lyapunov, only upper tiles are computed
+// and mirrored at the end (verify.py:299-300) with U = L^T (kernels.py:113-130).
+// Results agree with the statement-list executor to rounding (the tile-level
+// summation order differs), which the parity tests bound at 1e-10.
+//
+// Schedule: anti-diagonal d = I + J is solved at step d.  X_{I,k} / X_{k,J}
+// on diagonal d-1 are the LAST contributions any unsolved tile needs from
+// that diagonal's tiles in the same tile-row / tile-column... and every tile
+// of diagonal d-1 is needed only at step d, by exactly the tiles in its
+// row and column — so contributions are PULLED at step d from a one-diagonal
+// publish buffer (double-buffered), never stored as a full X in shared memory:
+//     step d:  (1) critical: tiles on diagonal d take their last two
+//                  contributions (4 DMMA) and are written to the publish slot
+//              (2) each 8-lane group solves one of the warp's diagonal-d
+//                  tiles in place (column-per-lane wavefront, shuffles);
+//                  the result (-X) is published and X streamed to HBM
+//              (3) bulk: every later tile takes its contributions from
+//                  diagonal d-1 (DMMA m8n8k4, accumulators in registers)
+//              one CTA-group barrier.
+// Residency: NW warps own a problem, accumulators of the unknown's tiles live
+// in registers (tile q of the diagonal-major order -> warp q % NW, slot
+// q / NW: balanced per diagonal); L (lower tiles) and U (upper tiles) in
+// shared memory, swizzled row-major 8x8 tiles so A, B and C fragments of
+// m8n8k4 and the solve's column walks are bank-conflict free.  n not a
+// multiple of 8 is padded exactly (identity diagonal, zero right-hand side).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "engine.cuh"
+
+#ifndef WAVE_SOLVE
+#define WAVE_SOLVE 1
+#endif
+namespace lagen {
+namespace wave {
+
+using eng::cp_async16;
+using eng::cp_async_commit;
+using eng::cp_async_wait;
+using eng::dmma;
+using eng::lane_id;
+
+// element (r, c) of a swizzled 8x8 tile: 16-byte pairs stay together, rows
+// 0/1 vs 2/3 (and 4/5 vs 6/7) swap column halves
+__device__ __forceinline__ int sw(int r, int c) { return r * 8 + (c ^ ((r & 2) << 1)); }
+
+template <int EQ, int N, int NW_, int PP_>
+struct WPol {
+  static_assert(EQ == 1 || EQ == 2, "wave engine: Lyapunov (1) or Sylvester (2)");
+  static constexpr int T = (N + 7) / 8;
+  static constexpr int NT = EQ == 2 ? T * T : T * (T + 1) / 2;  // unknown tiles
+  static constexpr int NW = NW_;
+  static constexpr int S = (NT + NW - 1) / NW;  // accumulator slots per warp
+  static constexpr int PP = PP_;
+  static constexpr int NLT = T * (T + 1) / 2;
+  static constexpr int NUT = EQ == 2 ? NLT : 0;
+  // L, U, publish (2 diagonals), L_II columns shifted for the solve (Lsh)
+  static constexpr int TILES = NLT + NUT + 2 * T + T;
+  static constexpr int SCR = NW * 4 * 64;          // per-group pivot reciprocals
+  static constexpr int SLOT = TILES * 64 + SCR + 2;  // doubles (+ flag)
+  static constexpr size_t SMEM = (size_t)PP * SLOT * 8;
+  static constexpr int THREADS = PP * NW * 32;
+  static_assert(T <= 16, "n <= 128");
+  static_assert((T + NW - 1) / NW <= 4, "at most 4 diagonal tiles per warp and step");
+};
+
+// 1 / a without the division subroutine (whose call would make the compiler
+// save the accumulator registers): rcp.approx + two Newton steps (~1 ulp)
+__device__ __forceinline__ double recip(double a) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  double e = fma(-a, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-a, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ int ltidx(int I, int J) { return I * (I + 1) / 2 + J; }  // I >= J
+__device__ __forceinline__ int utidx(int I, int J) { return J * (J + 1) / 2 + I; }  // I <= J
+
+// tile q of the diagonal-major order (diagonals ascending, I ascending)
+template <int EQ, int T>
+__device__ __forceinline__ int tile_of(int q) {
+  for (int d = 0; d <= 2 * T - 2; ++d) {
+    const int i0 = d - T + 1 > 0 ? d - T + 1 : 0;
+    const int i1 = EQ == 2 ? (d < T - 1 ? d : T - 1) : d / 2;
+    const int m = i1 - i0 + 1;
+    if (q < m) return ((i0 + q) << 4) | (d - i0 - q);
+    q -= m;
+  }
+  return 0xff;
+}
+
+// rows x 16-byte pairs of an n x n row-major operand into the lower (PART 0)
+// or upper (PART 1) tiles; pad units (outside n) get the identity
+template <int N, int T, int PART, int G>
+__device__ __forceinline__ void load_tri(double* tiles, const double* __restrict__ src, int rank) {
+  constexpr int NP = 8 * T, HP = NP / 2;
+  for (int u = rank; u < NP * HP; u += G) {
+    const int r = u / HP, cp = u - r * HP;
+    const int I = r >> 3, J = cp >> 2;
+    if (PART == 0 ? J > I : J < I) continue;
+    double* dst = tiles + (PART == 0 ? ltidx(I, J) : utidx(I, J)) * 64 + sw(r & 7, 2 * (cp & 3));
+    const int c = 2 * cp;
+    if (r < N && c < N) {
+      cp_async16(dst, src + r * N + c);
+    } else {
+      *reinterpret_cast<double2*>(dst) = make_double2(r == c ? 1.0 : 0.0, r == c + 1 ? 1.0 : 0.0);
+    }
+  }
+}
+
+template <int EQ, int N, int NW, int PP>
+__global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
+    wave_kernel(const double* __restrict__ Lg, const double* __restrict__ Ug, const double* __restrict__ Cg,
+                double* __restrict__ X, int* __restrict__ info, long long batch) {
+  using P = WPol<EQ, N, NW, PP>;
+  constexpr int T = P::T, S = P::S, G = NW * 32;
+  constexpr long long NN = (long long)N * N;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int grp = warp / NW, w = warp % NW, rank = threadIdx.x % G;
+  double* base = smem + (size_t)grp * P::SLOT;
+  double* Lt = base;
+  double* Ut = base + P::NLT * 64;
+  double* pub = base + (P::NLT + P::NUT) * 64;
+  double* Lsh = pub + 2 * T * 64;
+  double* scr = base + P::TILES * 64 + w * 256 + (lane >> 3) * 64 + (lane & 7) * 8;
+  int* flag = reinterpret_cast<int*>(base + P::TILES * 64 + P::SCR);
+  const int g = lane >> 2, t = lane & 3;
+  const int oA0 = sw(g, t), oA1 = sw(g, t + 4), oB0 = sw(t, g), oB1 = sw(t + 4, g), oC = sw(g, 2 * t);
+  auto gbar = [&]() {
+    if constexpr (NW == 1) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(G) : "memory");
+  };
+
+  // this warp's tiles: slot s -> packed (I << 4 | J) (tile q = s NW + w of
+  // the diagonal-major order); only the last slot can be empty (q >= NT)
+  unsigned tab[(S + 3) / 4];
+#pragma unroll
+  for (int i = 0; i < (S + 3) / 4; ++i) tab[i] = 0u;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int q = s * NW + w;
+    const unsigned ij = q < P::NT ? (unsigned)tile_of<EQ, T>(q) : 0u;
+    tab[s >> 2] |= ij << (8 * (s & 3));
+  }
+  const bool lastok = (S - 1) * NW + w < P::NT;
+  auto valid = [&](int s) { return s < S - 1 || lastok; };
+  auto tij = [&](int s) -> int { return (int)((tab[s >> 2] >> (8 * (s & 3))) & 0xff); };
+
+  const long long stride = (long long)gridDim.x * PP;
+  for (long long prob = (long long)blockIdx.x * PP + grp; prob < batch; prob += stride) {
+    const double* Lp = Lg + prob * NN;
+    const double* Up = Ug + prob * NN;
+    const double* Cp = Cg + prob * NN;
+    // coefficients -> shared memory (cp.async), right-hand side -> registers
+    load_tri<N, T, 0, G>(Lt, Lp, rank);
+    if constexpr (EQ == 2) load_tri<N, T, 1, G>(Ut, Up, rank);
+    cp_async_commit();
+    if (rank == 0) {
+      *flag = 0;
+      const long long nxt = prob + stride;
+      if (nxt < batch) {  // next problem's operands -> L2 while this one runs
+        const unsigned bytes = (unsigned)(NN * 8);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Lg + nxt * NN), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Cg + nxt * NN), "r"(bytes) : "memory");
+        if constexpr (EQ == 2)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Ug + nxt * NN), "r"(bytes) : "memory");
+      }
+    }
+    double a0[S], a1[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      a0[s] = a1[s] = 0.0;
+      if (!valid(s)) continue;
+      const int ij = tij(s);
+      const int I = ij >> 4, J = ij & 15;
+      const int r = 8 * I + g, c = 8 * J + 2 * t;
+      if (r < N && c < N) {
+        if (EQ == 1 && I == J && r > c) {  // symmetric right-hand side: upper triangle only
+          a0[s] = __ldg(Cp + (long long)c * N + r);
+          a1[s] = r > c + 1 ? __ldg(Cp + (long long)(c + 1) * N + r) : __ldg(Cp + (long long)r * N + c + 1);
+        } else {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(Cp + (long long)r * N + c));
+          a0[s] = v.x;
+          a1[s] = v.y;
+        }
+      }
+    }
+    cp_async_wait<0>();
+    gbar();
+    // Lsh[I][8 r + e] = L_II(r + e, r), e = 1..7 (0 below the tile): the solve
+    // reads one column of the diagonal block per step as 4 16-byte loads
+    for (int u = rank; u < T * 64; u += G) {
+      const int I = u >> 6, r = (u >> 3) & 7, e = u & 7;
+      Lsh[u] = (e >= 1 && r + e < 8) ? Lt[ltidx(I, I) * 64 + sw(r + e, r)] : 0.0;
+    }
+    gbar();
+    bool bad = false;
+
+    int q0 = 0;  // tiles on diagonals < d
+#pragma unroll 1
+    for (int d = 0; d <= 2 * T - 2; ++d) {
+      const int i0 = d - T + 1 > 0 ? d - T + 1 : 0;
+      const int m = (EQ == 2 ? (d < T - 1 ? d : T - 1) : d / 2) - i0 + 1;  // tiles on diagonal d
+      const int sc0 = (q0 - w + NW - 1) / NW, sc1 = (q0 + m - w + NW - 1) / NW;  // this warp's slots of d
+      const double* pv = pub + ((d + 1) & 1) * T * 64;  // diagonal d-1 (-X)
+      double* pc = pub + (d & 1) * T * 64;              // diagonal d
+      // contributions of diagonal d-1 into tile (I, J) (I + J >= d)
+      auto contrib = [&](double& c0, double& c1, int I, int J) {
+        if (J < d) {  // L_Ik X_kJ, k = d-1-J < I
+          const int k = d - 1 - J;
+          const double* A = Lt + ltidx(I, k) * 64;
+          const double* B = pv + k * 64;
+          dmma(c0, c1, A[oA0], B[oB0]);
+          dmma(c0, c1, A[oA1], B[oB1]);
+        }
+        if (I < d) {  // X_Ik U_kJ, k = d-1-I < J
+          const int k = d - 1 - I;
+          if constexpr (EQ == 2) {
+            const double* A = pv + I * 64;
+            const double* B = Ut + utidx(k, J) * 64;
+            dmma(c0, c1, A[oA0], B[oB0]);
+            dmma(c0, c1, A[oA1], B[oB1]);
+          } else {
+            // X_Ik: upper tile (I, k) or the transpose of (k, I); U_kJ = L_Jk^T
+            const double* A = pv + (I <= k ? I : k) * 64;
+            const int o0 = I <= k ? oA0 : oB0, o1 = I <= k ? oA1 : oB1;
+            const double* B = Lt + ltidx(J, k) * 64;
+            dmma(c0, c1, A[o0], B[oA0]);
+            dmma(c0, c1, A[o1], B[oA1]);
+          }
+        }
+      };
+      // (1) critical tiles of diagonal d: slot s <-> tile q = s NW + w,
+      //     position q - q0 along the diagonal
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if (s < sc0 || s >= sc1) continue;
+        const int I = i0 + s * NW + w - q0, J = d - I;
+        contrib(a0[s], a1[s], I, J);
+        *reinterpret_cast<double2*>(pc + I * 64 + oC) = make_double2(a0[s], a1[s]);
+      }
+      __syncwarp();
+      // (2) solve: group q of 8 lanes takes the q-th of them; lane c owns column c
+      const int ncrit = sc1 - sc0;
+      if (WAVE_SOLVE && ncrit > 0) {
+        const int qg = lane >> 3, c = lane & 7;
+        const bool live = qg < ncrit;
+        const int I = i0 + (sc0 + (live ? qg : 0)) * NW + w - q0, J = d - I;
+        double* Pt = pc + I * 64;
+        const double* Ld = Lt + ltidx(I, I) * 64;
+        const double* Ls = Lsh + I * 64;
+        // U_JJ (k, c):  sylvester U tile, lyapunov L_JJ^T
+        const double* Ud = EQ == 2 ? Ut + utidx(J, J) * 64 : Lt + ltidx(J, J) * 64;
+        auto uat = [&](int k) -> double { return EQ == 2 ? Ud[sw(k, c)] : Ud[sw(c, k)]; };
+        // y: column c of the right-hand side with row r = s - c handled at step
+        // s; y and the history h of computed values are circular buffers of 8
+        // (slot s & 7), so the step loop runs as 2 x 8 unrolled steps with
+        // static register indices and bounded live state.  y[s] is loaded
+        // when slot s & 7 frees up (step s - 8); rows outside 0..7 are 0.
+        auto yload = [&](int s) -> double {
+          const int r = s - c;
+          return (r >= 0 && r < 8) ? Pt[sw(r < 0 ? 0 : (r > 7 ? 7 : r), c)] : 0.0;
+        };
+        double y[8], h[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          y[s] = yload(s);
+          h[s] = 0.0;
+        }
+        double uc[8];
+        uc[0] = 0.0;
+#pragma unroll
+        for (int j = 1; j < 8; ++j) uc[j] = j <= c ? uat(c - j) : 0.0;
+        const double ucc = uat(c);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) scr[r] = recip(Ld[sw(r, r)] + ucc);
+        __syncwarp();
+        auto step = [&](int s, int u) {
+          const int r = s - c;
+          const bool act = r >= 0 && r < 8;
+          const int rc = r < 0 ? 0 : (r > 7 ? 7 : r);
+          const double piv = scr[rc];
+          const double2* lc = reinterpret_cast<const double2*>(Ls + 8 * rc);
+          const double2 l01 = lc[0], l23 = lc[1], l45 = lc[2], l67 = lc[3];
+          double v = y[u];
+          // row contributions: x(r, c - j) from lane c - j, computed j steps ago
+#pragma unroll
+          for (int j = 1; j < 8; ++j) {
+            const int src = (lane & ~7) | (c >= j ? c - j : c);
+            const double xv = __shfl_sync(0xffffffffu, h[(u - j) & 7], src);
+            v = fma(-xv, uc[j], v);
+          }
+          const double x = act ? v * piv : 0.0;
+          h[u] = x;
+          y[u] = yload(s + 8);
+          // own column: rows r + e take L(r + e, r) x
+          const double coef[8] = {0.0, l01.y, l23.x, l23.y, l45.x, l45.y, l67.x, l67.y};
+#pragma unroll
+          for (int e = 1; e < 8; ++e) y[(u + e) & 7] = fma(-coef[e], x, y[(u + e) & 7]);
+          if (act && live) Pt[sw(r, c)] = -x;
+        };
+#pragma unroll
+        for (int u = 0; u < 8; ++u) step(u, u);
+#pragma unroll
+        for (int u = 0; u < 7; ++u) step(8 + u, u);
+        __syncwarp();
+        if (EQ == 1 && live && I == J) {  // symmetric diagonal tile: lower := mirror of upper
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+            if (r > c) Pt[sw(r, c)] = Pt[sw(c, r)];  // upper entries are not written here
+        }
+        __syncwarp();
+        // stream X (= -published) to HBM: lane c writes row c of the tile
+        if (live) {
+          const int r = 8 * I + c;
+          double* Xp = X + prob * NN;
+#pragma unroll
+          for (int mm = 0; mm < 4; ++mm) {
+            const int col = 8 * J + 2 * mm;
+            if (r < N && col < N) {
+              const double2 v = *reinterpret_cast<const double2*>(Pt + sw(c, 2 * mm));
+              bad = bad || !isfinite(v.x) || !isfinite(v.y);
+              __stcs(reinterpret_cast<double2*>(Xp + (long long)r * N + col), make_double2(-v.x, -v.y));
+            }
+          }
+          if (EQ == 1 && I != J) {  // mirror tile (J, I): its row c is column c of this tile
+            const int r2 = 8 * J + c;
+#pragma unroll
+            for (int mm = 0; mm < 4; ++mm) {
+              const int col = 8 * I + 2 * mm;
+              if (r2 < N && col < N)
+                __stcs(reinterpret_cast<double2*>(Xp + (long long)r2 * N + col),
+                       make_double2(-Pt[sw(2 * mm, c)], -Pt[sw(2 * mm + 1, c)]));
+            }
+          }
+        }
+      }
+      // (3) bulk: every later tile takes diagonal d-1's contributions
+      if (d > 0) {
+        // opaque per step: keeps the compiler from hoisting S decoded tile
+        // coordinates / addresses out of the loop (register pressure)
+#pragma unroll
+        for (int i = 0; i < (S + 3) / 4; ++i) asm volatile("mov.b32 %0, %0;" : "+r"(tab[i]));
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          if (s < sc1 || !valid(s)) continue;
+          const int ij = tij(s);
+          contrib(a0[s], a1[s], ij >> 4, ij & 15);
+        }
+      }
+      q0 += m;
+      gbar();
+    }
+    if (bad) *flag = -1;
+    gbar();
+    if (rank == 0 && info) info[prob] = *flag;
+  }
+}
+
+}  // namespace wave
+}  // namespace lagen

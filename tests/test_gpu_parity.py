@@ -57,7 +57,7 @@ def test_golden_reference_vectors(eq):
         groups.setdefault((e["n"], e["variant"], e["b"]), []).append(e)
     from paper_1906_08613_b200 import _lib
     for (n, v, b), es in groups.items():
-      for engine in ("generic", "warp", "column", "dataflow", "rows"):
+      for engine in ("generic", "warp", "column", "dataflow", "rows", "wave"):
         if not _lib.engine_supported(EQ_CODES[eq], n, b, v, engine):
             continue
         ins = [np.stack([d[f"in_{e['case']}_{n}_{nm}"] for e in es]) for nm in EQ_INPUTS[eq]]
@@ -89,7 +89,7 @@ def test_every_variant_vs_oracle(eq, n, oracle_mod):
     assert (ref_info == 0).all()
     res_tol = 10 * n * EPS
     from paper_1906_08613_b200 import _lib
-    runs = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows") for v in vs for b in default_blocks(n)
+    runs = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows", "wave") for v in vs for b in default_blocks(n)
             if _lib.engine_supported(EQ_CODES[eq], n, b, v.index, e)]
     for v, b, engine in runs:
         if True:
@@ -139,11 +139,18 @@ def test_non_spd_and_nan_are_reported():
                 assert info.cpu().tolist() == [0, 0, bad + 1, 0], (n, v, engine)
         L, U, C = executor.generate("sylvester", n, seed=1, batch=3)
         C[1, 0, 0] = float("nan")
-        for engine in ("generic", "warp", "dataflow"):
+        for engine in ("generic", "warp", "dataflow", "wave"):
             if not _lib.engine_supported(2, n, 4, 13, engine):
                 continue
             _, info = executor.solve("sylvester", [L, U, C], variant=13, b=4, check=False, engine=engine)
             assert info.cpu().tolist() == [0, -1, 0], (n, engine)
+        L, S = executor.generate("lyapunov", n, seed=1, batch=3)
+        S[2, n - 1, n - 1] = float("inf")
+        for engine in ("generic", "warp", "dataflow", "wave"):
+            if not _lib.engine_supported(1, n, 4, 5, engine):
+                continue
+            _, info = executor.solve("lyapunov", [L, S], variant=5, b=4, check=False, engine=engine)
+            assert info.cpu().tolist() == [0, 0, -1], (n, engine)
     try:
         import lagen.errors
         with pytest.raises(lagen.errors.VerificationError):

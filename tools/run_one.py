@@ -12,11 +12,12 @@ ap.add_argument("--b", type=int, default=None)
 ap.add_argument("--variant", type=int, default=None)
 ap.add_argument("--batch", type=int, default=None)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--engine", default=None)
 a = ap.parse_args()
 torch.cuda.set_device(0)
 batch = a.batch or (1 << 28) // (8 * a.n * a.n)
 ins = executor.generate(a.eq, a.n, seed=a.n, batch=batch)
-plan = executor.Plan(a.eq, ins, variant=a.variant, b=a.b)
+plan = executor.Plan(a.eq, ins, variant=a.variant, b=a.b, engine=a.engine)
 for _ in range(a.reps):
     plan.launch()
 torch.cuda.synchronize()
