@@ -72,8 +72,15 @@ struct WPol {
   static constexpr size_t SMEM = (size_t)PP * SLOT * 8;
   static constexpr int THREADS = PP * NW * 32;
   static_assert(T <= 16, "n <= 128");
+  static_assert(S <= 40, "accumulator slots per warp");
   static_assert((T + NW - 1) / NW <= 4, "at most 4 diagonal tiles per warp and step");
 };
+
+// case list over accumulator slots 0..39 (S <= 40), used as Duff's device
+#define LAGEN_WAVE_SLOTS(X)                                                                                   \
+  X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) X(18) \
+  X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32) X(33) X(34) X(35)     \
+  X(36) X(37) X(38) X(39)
 
 // 1 / a without the division subroutine (whose call would make the compiler
 // save the accumulator registers): rcp.approx + two Newton steps (~1 ulp)
@@ -246,13 +253,19 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
       };
       // (1) critical tiles of diagonal d: slot s <-> tile q = s NW + w,
       //     position q - q0 along the diagonal
-#pragma unroll
-      for (int s = 0; s < S; ++s) {
-        if (s < sc0 || s >= sc1) continue;
-        const int I = i0 + s * NW + w - q0, J = d - I;
-        contrib(a0[s], a1[s], I, J);
-        *reinterpret_cast<double2*>(pc + I * 64 + oC) = make_double2(a0[s], a1[s]);
-      }
+      // (jump straight to slot sc0: a switch with fall-through over the
+      // unrolled slots, no per-slot tests for the slots already solved)
+#define LAGEN_WAVE_CRIT(k)                                                  \
+  case k:                                                                   \
+    if constexpr (k < S) {                                                  \
+      if (k >= sc1) break;                                                  \
+      const int I = i0 + k * NW + w - q0, J = d - I;                        \
+      contrib(a0[k], a1[k], I, J);                                          \
+      *reinterpret_cast<double2*>(pc + I * 64 + oC) = make_double2(a0[k], a1[k]); \
+    }                                                                       \
+    [[fallthrough]];
+      switch (sc0) { LAGEN_WAVE_SLOTS(LAGEN_WAVE_CRIT) default: break; }
+#undef LAGEN_WAVE_CRIT
       __syncwarp();
       // (2) solve: group q of 8 lanes takes the q-th of them; lane c owns column c
       const int ncrit = sc1 - sc0;
@@ -355,12 +368,16 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
         // coordinates / addresses out of the loop (register pressure)
 #pragma unroll
         for (int i = 0; i < (S + 3) / 4; ++i) asm volatile("mov.b32 %0, %0;" : "+r"(tab[i]));
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-          if (s < sc1 || !valid(s)) continue;
-          const int ij = tij(s);
-          contrib(a0[s], a1[s], ij >> 4, ij & 15);
-        }
+#define LAGEN_WAVE_BULK(k)                                  \
+  case k:                                                   \
+    if constexpr (k < S) {                                  \
+      if (k == S - 1 && !lastok) break;                     \
+      const int ij = tij(k);                                \
+      contrib(a0[k], a1[k], ij >> 4, ij & 15);              \
+    }                                                       \
+    [[fallthrough]];
+        switch (sc1) { LAGEN_WAVE_SLOTS(LAGEN_WAVE_BULK) default: break; }
+#undef LAGEN_WAVE_BULK
       }
       q0 += m;
       gbar();

@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--eqs", default=",".join(EQUATIONS))
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--engines", default="all")
+    ap.add_argument("--merge", action="store_true",
+                    help="keep an existing table entry unless a timed candidate beats its ms")
     ap.add_argument("--out", default=str(REPO / "paper_1906_08613_b200" / "dispatch_table.json"))
     ap.add_argument("--report", default=str(REPO / "gpurun_out" / "autotune_report.json"))
     args = ap.parse_args()
@@ -55,7 +57,7 @@ def main():
             rows = []
             ref_X = None
             from paper_1906_08613_b200 import _lib
-            cands = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows")
+            cands = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows", "wave")
                      for v in builtin_variants(eq) for b in default_blocks(n)
                      if _lib.engine_supported(_lib_eq(eq), n, b, v.index, e)]
             if args.engines != "all":
@@ -89,6 +91,11 @@ def main():
             if not good:
                 continue
             best = min(good, key=lambda r: (r["ms"], r["variant"], r["b"]))
+            old = table[eq].get(str(n))
+            if args.merge and old is not None and old.get("ms", 1e30) <= best["ms"]:
+                print(f"{eq} n={n}: keep {old} (candidate {best['engine']} {best['ms']:.4f} ms)", flush=True)
+                report[eq][str(n)] = rows
+                continue
             table[eq][str(n)] = {"variant": best["variant"], "b": best["b"], "engine": best["engine"],
                                  "ms": best["ms"]}
             report[eq][str(n)] = rows
