@@ -28,7 +28,7 @@ struct WCfg {
   static constexpr int mx(int a, int b) { return a > b ? a : b; }
   static constexpr int mn(int a, int b) { return a < b ? a : b; }
   static constexpr int NW = mx(mx(cdiv(T, 4), cdiv(NT, 32)), 1);
-  static constexpr int S = cdiv(NT, NW);
+  static constexpr int S = wave::WPol<EQ, N, NW, 1>::S;
   static constexpr int REGS = mn(255, 4 * S + 112);  // measured: ~112 beside the accumulators
   static constexpr int PPR = 65536 / (REGS * 32 * NW);
   static constexpr int SLOTB = (int)(wave::WPol<EQ, N, NW, 1>::SLOT * 8);
@@ -68,7 +68,11 @@ cudaError_t launch_wave_cfg(const LaunchArgs& a, cudaStream_t s) {
   const double* L = a.in[0];
   const double* U = EQ == 2 ? a.in[1] : a.in[0];
   const double* C = EQ == 2 ? a.in[2] : a.in[1];
-  kern<<<(unsigned)grid, P::THREADS, P::SMEM, s>>>(L, U, C, a.X, a.info, a.batch);
+  static const int mode = [] {
+    const char* e = std::getenv("LAGEN_WAVE_MODE");  // profiling switch, see wave_kernel
+    return e ? std::atoi(e) : 0;
+  }();
+  kern<<<(unsigned)grid, P::THREADS, P::SMEM, s>>>(L, U, C, a.X, a.info, a.batch, mode);
   return cudaGetLastError();
 }
 

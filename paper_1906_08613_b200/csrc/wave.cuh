@@ -61,14 +61,21 @@ struct WPol {
   static constexpr int T = (N + 7) / 8;
   static constexpr int NT = EQ == 2 ? T * T : T * (T + 1) / 2;  // unknown tiles
   static constexpr int NW = NW_;
-  static constexpr int S = (NT + NW - 1) / NW;  // accumulator slots per warp
+  // tile q -> warp (q / BLK) % NW: blocks of BLK consecutive tiles of the
+  // diagonal-major order per warp, so the diagonal-d solves land on few warps
+  // with full 8-lane groups (fewer solve passes per step)
+  static constexpr int BLK = 1;  // 4 measured slower (fewer warps carry the latency-bound solves)
+  static constexpr int S = BLK * (((NT + BLK - 1) / BLK + NW - 1) / NW);  // accumulator slots per warp
   static constexpr int PP = PP_;
   static constexpr int NLT = T * (T + 1) / 2;
   static constexpr int NUT = EQ == 2 ? NLT : 0;
-  // L, U, publish (2 diagonals), L_II columns shifted for the solve (Lsh)
-  static constexpr int TILES = NLT + NUT + 2 * T + T;
-  static constexpr int SCR = NW * 4 * 64;          // per-group pivot reciprocals
-  static constexpr int SLOT = TILES * 64 + SCR + 2;  // doubles (+ flag)
+  // L, U (64 doubles per tile), publish (2 diagonals, PS doubles per tile)
+  // and the L_II columns shifted for the solve (Lsh, 80 doubles per tile)
+  static constexpr int PS = 68;  // 544-byte pitch: the 4 groups' tiles start in different banks
+  static constexpr int TILES = NLT + NUT;
+  static constexpr int PUBD = 2 * T * PS + T * 80;
+  static constexpr int SCR = NW * 4 * 72;          // per-group pivot reciprocals (72: groups 1, 3 shift 8 banks)
+  static constexpr int SLOT = TILES * 64 + PUBD + SCR + 2;  // doubles (+ flag)
   static constexpr size_t SMEM = (size_t)PP * SLOT * 8;
   static constexpr int THREADS = PP * NW * 32;
   static_assert(T <= 16, "n <= 128");
@@ -131,7 +138,9 @@ __device__ __forceinline__ void load_tri(double* tiles, const double* __restrict
 template <int EQ, int N, int NW, int PP>
 __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
     wave_kernel(const double* __restrict__ Lg, const double* __restrict__ Ug, const double* __restrict__ Cg,
-                double* __restrict__ X, int* __restrict__ info, long long batch) {
+                double* __restrict__ X, int* __restrict__ info, long long batch, int mode) {
+  // mode (profiling only; results are wrong when set): bit 0 skips the
+  // diagonal solves, bit 1 the bulk contributions, bit 2 the critical ones
   using P = WPol<EQ, N, NW, PP>;
   constexpr int T = P::T, S = P::S, G = NW * 32;
   constexpr long long NN = (long long)N * N;
@@ -142,9 +151,10 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
   double* Lt = base;
   double* Ut = base + P::NLT * 64;
   double* pub = base + (P::NLT + P::NUT) * 64;
-  double* Lsh = pub + 2 * T * 64;
-  double* scr = base + P::TILES * 64 + w * 256 + (lane >> 3) * 64 + (lane & 7) * 8;
-  int* flag = reinterpret_cast<int*>(base + P::TILES * 64 + P::SCR);
+  constexpr int PS = P::PS;
+  double* Lsh = pub + 2 * T * PS;
+  double* scr = base + P::TILES * 64 + P::PUBD + w * 288 + (lane >> 3) * 72 + (lane & 7) * 8;
+  int* flag = reinterpret_cast<int*>(base + P::TILES * 64 + P::PUBD + P::SCR);
   const int g = lane >> 2, t = lane & 3;
   const int oA0 = sw(g, t), oA1 = sw(g, t + 4), oB0 = sw(t, g), oB1 = sw(t + 4, g), oC = sw(g, 2 * t);
   auto gbar = [&]() {
@@ -152,19 +162,25 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
     else asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(G) : "memory");
   };
 
-  // this warp's tiles: slot s -> packed (I << 4 | J) (tile q = s NW + w of
-  // the diagonal-major order); only the last slot can be empty (q >= NT)
+  // this warp's tiles: slot s -> packed (I << 4 | J) of tile qof(s) of the
+  // diagonal-major order; slots past NT (a suffix) are empty
+  constexpr int BLK = P::BLK;
+  auto qof = [&](int s) { return ((s / BLK) * NW + w) * BLK + s % BLK; };
+  // number of this warp's tiles among q < x
+  auto cnt = [&](int x) {
+    const int B = x / BLK;
+    return BLK * ((B - w + NW - 1) / NW) + ((B % NW == w) ? x % BLK : 0);
+  };
   unsigned tab[(S + 3) / 4];
 #pragma unroll
   for (int i = 0; i < (S + 3) / 4; ++i) tab[i] = 0u;
 #pragma unroll
   for (int s = 0; s < S; ++s) {
-    const int q = s * NW + w;
+    const int q = qof(s);
     const unsigned ij = q < P::NT ? (unsigned)tile_of<EQ, T>(q) : 0u;
     tab[s >> 2] |= ij << (8 * (s & 3));
   }
-  const bool lastok = (S - 1) * NW + w < P::NT;
-  auto valid = [&](int s) { return s < S - 1 || lastok; };
+  auto valid = [&](int s) { return qof(s) < P::NT; };
   auto tij = [&](int s) -> int { return (int)((tab[s >> 2] >> (8 * (s & 3))) & 0xff); };
 
   const long long stride = (long long)gridDim.x * PP;
@@ -208,11 +224,12 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
     }
     cp_async_wait<0>();
     gbar();
-    // Lsh[I][8 r + e] = L_II(r + e, r), e = 1..7 (0 below the tile): the solve
-    // reads one column of the diagonal block per step as 4 16-byte loads
+    // Lsh[I][10 r + e] = L_II(r + e, r), e = 1..7 (0 below the tile): the solve
+    // reads one column of the diagonal block per step as 4 16-byte loads; the
+    // 80-byte row pitch puts the 8 lanes' rows on disjoint banks
     for (int u = rank; u < T * 64; u += G) {
       const int I = u >> 6, r = (u >> 3) & 7, e = u & 7;
-      Lsh[u] = (e >= 1 && r + e < 8) ? Lt[ltidx(I, I) * 64 + sw(r + e, r)] : 0.0;
+      Lsh[I * 80 + r * 10 + e] = (e >= 1 && r + e < 8) ? Lt[ltidx(I, I) * 64 + sw(r + e, r)] : 0.0;
     }
     gbar();
     bool bad = false;
@@ -222,28 +239,28 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
     for (int d = 0; d <= 2 * T - 2; ++d) {
       const int i0 = d - T + 1 > 0 ? d - T + 1 : 0;
       const int m = (EQ == 2 ? (d < T - 1 ? d : T - 1) : d / 2) - i0 + 1;  // tiles on diagonal d
-      const int sc0 = (q0 - w + NW - 1) / NW, sc1 = (q0 + m - w + NW - 1) / NW;  // this warp's slots of d
-      const double* pv = pub + ((d + 1) & 1) * T * 64;  // diagonal d-1 (-X)
-      double* pc = pub + (d & 1) * T * 64;              // diagonal d
+      const int sc0 = cnt(q0), sc1 = cnt(q0 + m);  // this warp's slots of diagonal d
+      const double* pv = pub + ((d + 1) & 1) * T * PS;  // diagonal d-1 (-X)
+      double* pc = pub + (d & 1) * T * PS;              // diagonal d
       // contributions of diagonal d-1 into tile (I, J) (I + J >= d)
       auto contrib = [&](double& c0, double& c1, int I, int J) {
         if (J < d) {  // L_Ik X_kJ, k = d-1-J < I
           const int k = d - 1 - J;
           const double* A = Lt + ltidx(I, k) * 64;
-          const double* B = pv + k * 64;
+          const double* B = pv + k * PS;
           dmma(c0, c1, A[oA0], B[oB0]);
           dmma(c0, c1, A[oA1], B[oB1]);
         }
         if (I < d) {  // X_Ik U_kJ, k = d-1-I < J
           const int k = d - 1 - I;
           if constexpr (EQ == 2) {
-            const double* A = pv + I * 64;
+            const double* A = pv + I * PS;
             const double* B = Ut + utidx(k, J) * 64;
             dmma(c0, c1, A[oA0], B[oB0]);
             dmma(c0, c1, A[oA1], B[oB1]);
           } else {
             // X_Ik: upper tile (I, k) or the transpose of (k, I); U_kJ = L_Jk^T
-            const double* A = pv + (I <= k ? I : k) * 64;
+            const double* A = pv + (I <= k ? I : k) * PS;
             const int o0 = I <= k ? oA0 : oB0, o1 = I <= k ? oA1 : oB1;
             const double* B = Lt + ltidx(J, k) * 64;
             dmma(c0, c1, A[o0], B[oA0]);
@@ -259,23 +276,23 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
   case k:                                                                   \
     if constexpr (k < S) {                                                  \
       if (k >= sc1) break;                                                  \
-      const int I = i0 + k * NW + w - q0, J = d - I;                        \
+      const int I = i0 + qof(k) - q0, J = d - I;                            \
       contrib(a0[k], a1[k], I, J);                                          \
-      *reinterpret_cast<double2*>(pc + I * 64 + oC) = make_double2(a0[k], a1[k]); \
+      *reinterpret_cast<double2*>(pc + I * PS + oC) = make_double2(a0[k], a1[k]); \
     }                                                                       \
     [[fallthrough]];
-      switch (sc0) { LAGEN_WAVE_SLOTS(LAGEN_WAVE_CRIT) default: break; }
+      if (!(mode & 4)) switch (sc0) { LAGEN_WAVE_SLOTS(LAGEN_WAVE_CRIT) default: break; }
 #undef LAGEN_WAVE_CRIT
       __syncwarp();
       // (2) solve: group q of 8 lanes takes the q-th of them; lane c owns column c
       const int ncrit = sc1 - sc0;
-      if (WAVE_SOLVE && ncrit > 0) {
+      if (WAVE_SOLVE && ncrit > 0 && !(mode & 1)) {
         const int qg = lane >> 3, c = lane & 7;
         const bool live = qg < ncrit;
-        const int I = i0 + (sc0 + (live ? qg : 0)) * NW + w - q0, J = d - I;
-        double* Pt = pc + I * 64;
+        const int I = i0 + qof(sc0 + (live ? qg : 0)) - q0, J = d - I;
+        double* Pt = pc + I * PS;
         const double* Ld = Lt + ltidx(I, I) * 64;
-        const double* Ls = Lsh + I * 64;
+        const double* Ls = Lsh + I * 80;
         // U_JJ (k, c):  sylvester U tile, lyapunov L_JJ^T
         const double* Ud = EQ == 2 ? Ut + utidx(J, J) * 64 : Lt + ltidx(J, J) * 64;
         auto uat = [&](int k) -> double { return EQ == 2 ? Ud[sw(k, c)] : Ud[sw(c, k)]; };
@@ -302,28 +319,35 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
 #pragma unroll
         for (int r = 0; r < 8; ++r) scr[r] = recip(Ld[sw(r, r)] + ucc);
         __syncwarp();
+        // one wavefront step; the dependence on the previous step is kept to
+        // shfl(x(r, c-1)) -> FMA -> MUL and push(x(r-1, c)) -> ADD -> FMA -> MUL:
+        // contributions of values >= 2 steps old are summed off that chain
         auto step = [&](int s, int u) {
           const int r = s - c;
           const bool act = r >= 0 && r < 8;
           const int rc = r < 0 ? 0 : (r > 7 ? 7 : r);
-          const double piv = scr[rc];
-          const double2* lc = reinterpret_cast<const double2*>(Ls + 8 * rc);
+          const double piv = act ? scr[rc] : 0.0;
+          const double2* lc = reinterpret_cast<const double2*>(Ls + 10 * rc);
           const double2 l01 = lc[0], l23 = lc[1], l45 = lc[2], l67 = lc[3];
-          double v = y[u];
           // row contributions: x(r, c - j) from lane c - j, computed j steps ago
+          double t0 = 0.0, t1 = 0.0;
 #pragma unroll
-          for (int j = 1; j < 8; ++j) {
+          for (int j = 2; j < 8; ++j) {
             const int src = (lane & ~7) | (c >= j ? c - j : c);
             const double xv = __shfl_sync(0xffffffffu, h[(u - j) & 7], src);
-            v = fma(-xv, uc[j], v);
+            if (j & 1) t1 = fma(xv, uc[j], t1);
+            else t0 = fma(xv, uc[j], t0);
           }
-          const double x = act ? v * piv : 0.0;
+          const double x1 = __shfl_sync(0xffffffffu, h[(u - 1) & 7], (lane & ~7) | (c >= 1 ? c - 1 : c));
+          double v = y[u] - (t0 + t1);
+          v = fma(-x1, uc[1], v);
+          const double x = v * piv;
           h[u] = x;
-          y[u] = yload(s + 8);
-          // own column: rows r + e take L(r + e, r) x
+          // own column: rows r + e take L(r + e, r) x (row r + 1 first: next step)
           const double coef[8] = {0.0, l01.y, l23.x, l23.y, l45.x, l45.y, l67.x, l67.y};
 #pragma unroll
           for (int e = 1; e < 8; ++e) y[(u + e) & 7] = fma(-coef[e], x, y[(u + e) & 7]);
+          y[u] = yload(s + 8);
           if (act && live) Pt[sw(r, c)] = -x;
         };
 #pragma unroll
@@ -363,7 +387,7 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
         }
       }
       // (3) bulk: every later tile takes diagonal d-1's contributions
-      if (d > 0) {
+      if (d > 0 && !(mode & 2)) {
         // opaque per step: keeps the compiler from hoisting S decoded tile
         // coordinates / addresses out of the loop (register pressure)
 #pragma unroll
@@ -371,7 +395,7 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
 #define LAGEN_WAVE_BULK(k)                                  \
   case k:                                                   \
     if constexpr (k < S) {                                  \
-      if (k == S - 1 && !lastok) break;                     \
+      if (!valid(k)) break;                                 \
       const int ij = tij(k);                                \
       contrib(a0[k], a1[k], ij >> 4, ij & 15);              \
     }                                                       \
