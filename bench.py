@@ -464,7 +464,7 @@ def main():
                        "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                        "steps": e2e_steps,
                        "path": "executor.solve_host -> lagen_b200_execute_host_engine (pinned host buffers, "
-                               "chunked H2D/solve/D2H over two streams)"}
+                               "chunked H2D/solve/D2H over four persistent streams)"}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(eq, cases, budget_s=args.cpu_budget,
                                             inputs_from=[p.inputs for p in res["plans"]])

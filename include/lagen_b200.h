@@ -144,7 +144,8 @@ int lagen_b200_engine_supported(int eq, int n, int b, int variant, int engine);
 
 /* Same, but every buffer is in HOST memory (pinned for full overlap).  The
  * batch is streamed through the device in chunks, H2D copy / solve / D2H copy
- * pipelined over two streams; synchronous on return. */
+ * pipelined over four streams with persistent staging buffers (PCIe
+ * bidirectional-bound); synchronous on return. */
 int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
                             long long batch, const double* const* h_inputs,
                             double* h_X, int* h_info);

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "inst_index.h"
@@ -348,6 +349,45 @@ int lagen_b200_sylvester(int variant, int n, int b, long long batch, const doubl
 // Host-buffer pipeline: chunks of the batch cycle through NS device buffer
 // sets on NS streams so the H2D engine, the SMs and the D2H engine all stay
 // busy (with 2 sets the H2D of chunk c+2 would wait for the D2H of chunk c).
+// Streams and staging buffers persist across calls (per device, grown on
+// demand, one caller at a time): a sweep of many sizes pays no per-call
+// stream creation / allocation, and no pool release between calls.
+namespace {
+constexpr int kNS = 4;
+struct HostPipe {
+  int dev = -1;
+  cudaStream_t st[kNS] = {nullptr};
+  double* d_in[kNS][3] = {{nullptr}};
+  double* d_X[kNS] = {nullptr};
+  int* d_info[kNS] = {nullptr};
+  size_t cap_bytes = 0, cap_info = 0;
+  cudaError_t reserve(size_t bytes, size_t info_bytes) {
+    if (bytes <= cap_bytes && info_bytes <= cap_info) return cudaSuccess;
+    for (int k = 0; k < kNS; ++k) {
+      if (st[k]) cudaStreamSynchronize(st[k]);
+      for (int i = 0; i < 3; ++i) cudaFree(d_in[k][i]), d_in[k][i] = nullptr;
+      cudaFree(d_X[k]), d_X[k] = nullptr;
+      cudaFree(d_info[k]), d_info[k] = nullptr;
+    }
+    cap_bytes = cap_info = 0;
+    cudaError_t err = cudaSuccess;
+    for (int k = 0; k < kNS && err == cudaSuccess; ++k) {
+      if (!st[k]) err = cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
+      for (int i = 0; i < 3 && err == cudaSuccess; ++i) err = cudaMalloc(&d_in[k][i], bytes);
+      if (err == cudaSuccess) err = cudaMalloc(&d_X[k], bytes);
+      if (err == cudaSuccess) err = cudaMalloc(&d_info[k], info_bytes);
+    }
+    if (err == cudaSuccess) {
+      cap_bytes = bytes;
+      cap_info = info_bytes;
+    }
+    return err;
+  }
+};
+std::mutex g_pipe_mu;
+HostPipe g_pipe[64];
+}  // namespace
+
 int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                             const double* const* h_inputs, double* h_X, int* h_info) {
   return lagen_b200_execute_host_engine(eq, stmts, nstmts, n, b, batch, h_inputs, h_X, h_info, LAGEN_ENGINE_AUTO);
@@ -355,7 +395,6 @@ int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, 
 
 int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                    const double* const* h_inputs, double* h_X, int* h_info, int engine) {
-  constexpr int NS = 4;
   if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_WAVE) return fail(LAGEN_EINVAL, "unknown engine");
   int rc = check_common(eq, n, b, batch);
   if (rc) return rc;
@@ -366,49 +405,39 @@ int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, 
   const int nin = eq_ninputs(eq);
   for (int i = 0; i < nin; ++i)
     if (!h_inputs[i]) return fail(LAGEN_EINVAL, "null input buffer");
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return cuda_fail(err, "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return fail(LAGEN_EINVAL, "device index out of range");
   const size_t prob_bytes = sizeof(double) * (size_t)n * n;
   // ~16 MiB of input per chunk and operand, at least one problem
   long long chunk = (16ll << 20) / (long long)prob_bytes;
   if (chunk < 1) chunk = 1;
+  std::lock_guard<std::mutex> lock(g_pipe_mu);
+  HostPipe& hp = g_pipe[dev];
+  err = hp.reserve((size_t)chunk * prob_bytes, (size_t)chunk * sizeof(int));
+  if (err != cudaSuccess) return cuda_fail(err, "host pipeline setup");
   if (chunk > batch) chunk = batch;
-  cudaStream_t st[NS] = {nullptr};
-  double* d_in[NS][3] = {{nullptr}};
-  double* d_X[NS] = {nullptr};
-  int* d_info[NS] = {nullptr};
-  cudaError_t err = cudaSuccess;
-  const long long nchunks = (batch + chunk - 1) / chunk;
-  const int ns = nchunks < NS ? (int)nchunks : NS;
-  for (int k = 0; k < ns && err == cudaSuccess; ++k) {
-    err = cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
-    for (int i = 0; i < nin && err == cudaSuccess; ++i) err = cudaMallocAsync(&d_in[k][i], chunk * prob_bytes, st[k]);
-    if (err == cudaSuccess) err = cudaMallocAsync(&d_X[k], chunk * prob_bytes, st[k]);
-    if (err == cudaSuccess && h_info) err = cudaMallocAsync(&d_info[k], chunk * sizeof(int), st[k]);
-  }
   int status = LAGEN_OK;
-  if (err != cudaSuccess) status = cuda_fail(err, "host pipeline setup");
   for (long long c0 = 0, it = 0; status == LAGEN_OK && c0 < batch; c0 += chunk, ++it) {
-    const int k = (int)(it % ns);
+    const int k = (int)(it % kNS);
     const long long cnt = (batch - c0) < chunk ? (batch - c0) : chunk;
     for (int i = 0; i < nin && err == cudaSuccess; ++i)
-      err = cudaMemcpyAsync(d_in[k][i], h_inputs[i] + c0 * n * n, cnt * prob_bytes, cudaMemcpyHostToDevice, st[k]);
+      err = cudaMemcpyAsync(hp.d_in[k][i], h_inputs[i] + c0 * n * n, cnt * prob_bytes, cudaMemcpyHostToDevice,
+                            hp.st[k]);
     if (err != cudaSuccess) { status = cuda_fail(err, "H2D"); break; }
-    const double* ins[3] = {d_in[k][0], d_in[k][1], d_in[k][2]};
-    status = lagen_b200_execute_engine(eq, stmts, nstmts, n, b, cnt, ins, d_X[k], d_info[k], st[k], engine);
+    const double* ins[3] = {hp.d_in[k][0], hp.d_in[k][1], hp.d_in[k][2]};
+    status = lagen_b200_execute_engine(eq, stmts, nstmts, n, b, cnt, ins, hp.d_X[k], h_info ? hp.d_info[k] : nullptr,
+                                       hp.st[k], engine);
     if (status != LAGEN_OK) break;
-    err = cudaMemcpyAsync(h_X + c0 * n * n, d_X[k], cnt * prob_bytes, cudaMemcpyDeviceToHost, st[k]);
+    err = cudaMemcpyAsync(h_X + c0 * n * n, hp.d_X[k], cnt * prob_bytes, cudaMemcpyDeviceToHost, hp.st[k]);
     if (err == cudaSuccess && h_info)
-      err = cudaMemcpyAsync(h_info + c0, d_info[k], cnt * sizeof(int), cudaMemcpyDeviceToHost, st[k]);
+      err = cudaMemcpyAsync(h_info + c0, hp.d_info[k], cnt * sizeof(int), cudaMemcpyDeviceToHost, hp.st[k]);
     if (err != cudaSuccess) { status = cuda_fail(err, "D2H"); break; }
   }
-  for (int k = 0; k < ns; ++k) {
-    if (!st[k]) continue;
-    for (int i = 0; i < 3; ++i)
-      if (d_in[k][i]) cudaFreeAsync(d_in[k][i], st[k]);
-    if (d_X[k]) cudaFreeAsync(d_X[k], st[k]);
-    if (d_info[k]) cudaFreeAsync(d_info[k], st[k]);
-    cudaError_t e2 = cudaStreamSynchronize(st[k]);
+  for (int k = 0; k < kNS; ++k) {
+    cudaError_t e2 = cudaStreamSynchronize(hp.st[k]);
     if (e2 != cudaSuccess && status == LAGEN_OK) status = cuda_fail(e2, "host pipeline sync");
-    cudaStreamDestroy(st[k]);
   }
   return status;
 }
