@@ -63,7 +63,7 @@ EXPORTED = (
     "lagen_b200_execute_engine", "lagen_b200_warp_supported", "lagen_b200_engine_supported",
     "lagen_b200_execute_profile",
 )
-ENGINES = {"auto": 0, "generic": 1, "warp": 2, "column": 3, "dataflow": 4, "rows": 5, "wave": 6}
+ENGINES = {"auto": 0, "generic": 1, "warp": 2, "column": 3, "dataflow": 4, "rows": 5, "wave": 6, "rowspad": 7}
 
 
 def engine_supported(eq_code, n, b, variant, engine):

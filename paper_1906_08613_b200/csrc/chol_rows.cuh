@@ -87,12 +87,19 @@ struct KRow {
 // row-major n x n (upper part) -> packed rows, cp.async 16-byte units; full
 // rows are walked (division by the compile-time half-width) and the chunks
 // left of each row's first stored column are skipped
-template <int N, int G>
+// NR < N: the real problem is NR x NR (ld NR), padded to N with the identity
+// (A_pad = diag(A, I) -> X_pad = diag(X, I), exactly)
+template <int N, int G, int NR = N>
 __device__ __forceinline__ void load_rows(double* xs, const double* __restrict__ src, int rank) {
   constexpr int H = N / 2;
   for (int u = rank; u < N * H; u += G) {
     const int r = u / H, c = 2 * (u - r * H);
-    if (c >= 4 * (r >> 2)) cp_async16(xs + Rows<N>::at(r, c), src + r * N + c);
+    if (c >= 4 * (r >> 2)) {
+      if (NR == N || (r < NR && c < NR))
+        cp_async16(xs + Rows<N>::at(r, c), src + r * NR + c);
+      else
+        *reinterpret_cast<double2*>(xs + Rows<N>::at(r, c)) = make_double2(r == c ? 1.0 : 0.0, r == c + 1 ? 1.0 : 0.0);
+    }
   }
 }
 
@@ -343,14 +350,15 @@ __device__ __forceinline__ void trsm(double* xs, int r0, const double* rsb, int 
 }
 
 // block row [r0, r0 + B) -> X (row-major, zeros left of the diagonal)
-template <int N, int B>
+template <int N, int B, int NR = N>
 __device__ __forceinline__ void store_rows(double* __restrict__ dst, const double* xs, int r0, int rank, int nthr) {
-  constexpr int H = N / 2;  // 16-byte units per row
-  for (int u = rank; u < B * H; u += nthr) {
+  constexpr int H = NR / 2;  // 16-byte units per (real) row
+  const int nb = r0 + B <= NR ? B : NR - r0;  // real rows of this block row
+  for (int u = rank; u < nb * H; u += nthr) {
     const int i = u / H, r = r0 + i, c = 2 * (u - i * H);
     double2 v = make_double2(0.0, 0.0);
     if (c >= 4 * (r >> 2)) v = *reinterpret_cast<const double2*>(xs + Rows<N>::at(r, c));
-    __stcs(reinterpret_cast<double2*>(dst + r * N + c), v);
+    __stcs(reinterpret_cast<double2*>(dst + r * NR + c), v);
   }
 }
 
@@ -370,7 +378,7 @@ constexpr unsigned char kRowsMode[2][33] = {{1, 1, 1, 1, 1, 1, 1, 1, 1, 13, 1, 1
 inline int rows_wg(int n, int b) { return kRowsWG[b == 8][n / 4]; }
 inline int default_mode(int n, int b) { return kRowsMode[b == 8][n / 4]; }
 
-template <int N, int B, int WG_>
+template <int N, int B, int WG_, int NR = N>
 __global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)
     chol_rows_kernel(const double* __restrict__ A, double* __restrict__ X, int* __restrict__ info,
                      long long batch, int mode) {
@@ -394,11 +402,11 @@ __global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)
   const int subbar = (WG > 2 && 1 + P::P + gr.id <= 15) ? 1 + P::P + gr.id : 0;
   if (!subbar) gr.scr = (WG > 2) ? nullptr : gr.scr;  // split-K needs the sub-group barrier
   auto slot_at = [&](int d) { return smem + ((size_t)gr.id * P::DB + (d % P::DB)) * P::SLOT; };
-  constexpr long long NN = (long long)N * N;
+  constexpr long long NN = (long long)NR * NR;
   const long long stride = (long long)gridDim.x * P::P;
   long long prob = (long long)blockIdx.x * P::P + gr.id;
   if (prob < batch) {
-    load_rows<N, G>(slot_at(0), A + prob * NN, gr.rank);
+    load_rows<N, G, NR>(slot_at(0), A + prob * NN, gr.rank);
     cp_async_commit();
   }
   int cur = 0;
@@ -408,7 +416,7 @@ __global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)
     double* xs = slot_at(cur);
     if constexpr (P::DB == 2) {
       if (nxt < batch) {
-        load_rows<N, G>(slot_at(cur ^ 1), A + nxt * NN, gr.rank);
+        load_rows<N, G, NR>(slot_at(cur ^ 1), A + nxt * NN, gr.rank);
         cp_async_commit();
         cp_async_wait<1>();
       } else {
@@ -444,7 +452,7 @@ __global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)
         __syncwarp();
         trsm<N, B>(xs, r0, gr.rsb, gr.rank, G);
         __syncwarp();
-        store_rows<N, B>(X + off, xs, r0, gr.rank, G);
+        store_rows<N, B, NR>(X + off, xs, r0, gr.rank, G);
       } else {
         // level A.  warp 0: the last block row's S1 contribution (K = B; the
         // rows above were applied one iteration ahead), then the leaf.
@@ -460,10 +468,10 @@ __global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)
           if (r0 > 0) s1_tile<N, B>(xs, r0, ahead ? (r0 - B) >> 2 : 0, r0 >> 2);
           __syncwarp();
           leaf<N, B>(xs, r0, gr.rsb, &flag);
-          if (w0_store && r0 > 0) store_rows<N, B>(X + off, xs, r0 - B, lane, 32);
+          if (w0_store && r0 > 0) store_rows<N, B, NR>(X + off, xs, r0 - B, lane, 32);
           if (ahead && w0_look && r0 + B < N && r0 > 0) s1_tile<N, B>(xs, r0 + B, 0, r0 >> 2);
         } else {
-          if (!w0_store && r0 > 0) store_rows<N, B>(X + off, xs, r0 - B, gr.rank - 32, 32 * (WG - 1));
+          if (!w0_store && r0 > 0) store_rows<N, B, NR>(X + off, xs, r0 - B, gr.rank - 32, 32 * (WG - 1));
           if constexpr (WG == 2) {
             s3<N, B, WG>(xs, r0, 0, 1, gr, 0, 32, split_mode);
           } else {
@@ -480,14 +488,14 @@ __global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)
         tick(3);
       }
     }
-    if constexpr (WG > 1) store_rows<N, B>(X + off, xs, N - B, gr.rank, G);
+    if constexpr (WG > 1) store_rows<N, B, NR>(X + off, xs, N - B, gr.rank, G);
     if (gr.wig == 0 && lane == 0 && flag) gflag[gr.id] = flag;
     gsync<WG>(gr);
     if (info && gr.rank == 0) info[prob] = gflag[gr.id];
     if constexpr (P::DB == 1) {
       gsync<WG>(gr);  // slot reads done before it is refilled
       if (nxt < batch) {
-        load_rows<N, G>(slot_at(0), A + nxt * NN, gr.rank);
+        load_rows<N, G, NR>(slot_at(0), A + nxt * NN, gr.rank);
         cp_async_commit();
       }
     } else {

@@ -74,6 +74,17 @@ const RowsEntry* find_rows(int eq, int n, int b, int variant) {
   return nullptr;
 }
 
+// padded rows engine: Cholesky v1, n = 4 (mod 8), as the b = 8 kernel of n + 4
+const RowsEntry* find_rows_pad(int eq, int n, int b, int variant) {
+  if (eq != 0 || variant != 1 || b != 4) return nullptr;
+  for (int p = 0; p < kRowsPadParts; ++p) {
+    const RowsPadTable& t = kRowsPadTables[p];
+    for (int i = 0; i < *t.n; ++i)
+      if (t.e[i].n == n) return &t.e[i];
+  }
+  return nullptr;
+}
+
 // wave engine: Lyapunov v5 / Sylvester v13 (the right-looking variants whose
 // tile-level order it follows, wave.cuh), any block size the variant runs at
 const WaveEntry* find_wave(int eq, int n, int b, int variant) {
@@ -250,6 +261,7 @@ int lagen_b200_engine_supported(int eq, int n, int b, int variant, int engine) {
     case LAGEN_ENGINE_DATAFLOW: return find_df(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_ROWS: return find_rows(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_WAVE: return find_wave(eq, n, b, variant) ? 1 : 0;
+    case LAGEN_ENGINE_ROWS_PAD: return find_rows_pad(eq, n, b, variant) ? 1 : 0;
   }
   return 0;
 }
@@ -267,7 +279,7 @@ int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n
 int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                const double* const* inputs, double* X, int* info, void* stream, int engine,
                                unsigned long long* d_prof) {
-  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_WAVE) return fail(LAGEN_EINVAL, "unknown engine");
+  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWS_PAD) return fail(LAGEN_EINVAL, "unknown engine");
   int rc = check_common(eq, n, b, batch);
   if (rc) return rc;
   rc = validate(eq, stmts, nstmts);
@@ -309,7 +321,11 @@ int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int 
         (engine == LAGEN_ENGINE_WAVE || (engine == LAGEN_ENGINE_AUTO && n >= 16)) ? find_wave(eq, n, b, v) : nullptr;
     if (engine == LAGEN_ENGINE_WAVE && !wv)
       return fail(LAGEN_EUNSUPPORTED, "no wave-engine instance for this (variant, n, b)");
-    if (wv) fn = wv->launch;
+    const RowsEntry* rp = (engine == LAGEN_ENGINE_ROWS_PAD) ? find_rows_pad(eq, n, b, v) : nullptr;
+    if (engine == LAGEN_ENGINE_ROWS_PAD && !rp)
+      return fail(LAGEN_EUNSUPPORTED, "no padded rows-engine instance for this (variant, n, b)");
+    if (rp) fn = rp->launch;
+    else if (wv) fn = wv->launch;
     else if (st) fn = st->launch;
     else if (d) fn = d->launch;
     else if (c) fn = c->launch;
@@ -395,7 +411,7 @@ int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, 
 
 int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                    const double* const* h_inputs, double* h_X, int* h_info, int engine) {
-  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_WAVE) return fail(LAGEN_EINVAL, "unknown engine");
+  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWS_PAD) return fail(LAGEN_EINVAL, "unknown engine");
   int rc = check_common(eq, n, b, batch);
   if (rc) return rc;
   rc = validate(eq, stmts, nstmts);

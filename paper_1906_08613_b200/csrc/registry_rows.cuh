@@ -14,7 +14,7 @@ struct RowsEntry {
   LaunchFn launch;
 };
 
-template <int N, int B, int WG>
+template <int N, int B, int WG, int NR = N>
 cudaError_t launch_rows_wg(const LaunchArgs& a, cudaStream_t s, int mode) {
   using P = cr::RPolicy<N, WG>;
   static std::atomic<unsigned long long> configured{0};
@@ -24,7 +24,7 @@ cudaError_t launch_rows_wg(const LaunchArgs& a, cudaStream_t s, int mode) {
   cudaError_t err = cudaGetDevice(&dev);
   if (err != cudaSuccess) return err;
   const unsigned long long bit = 1ull << (dev & 63);
-  auto kern = cr::chol_rows_kernel<N, B, WG>;
+  auto kern = cr::chol_rows_kernel<N, B, WG, NR>;
   if (!(configured.load(std::memory_order_acquire) & bit)) {
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
     if (err != cudaSuccess) return err;
@@ -62,6 +62,30 @@ cudaError_t launch_rows(const LaunchArgs& a, cudaStream_t s) {
   if (wg == 2) return launch_rows_wg<N, B, 2>(a, s, mode);
   return launch_rows_wg<N, B, 4>(a, s, mode);
 }
+
+// n = 4 (mod 8): the b = 8 kernel of size n + 4 on the identity-padded
+// problem (diag(A, I) = diag(X, I)^T diag(X, I), exact), reading and writing
+// only the real n x n entries — the b = 8 schedule is the faster one
+// (half the iterations of b = 4) at every measured size
+template <int NR>
+cudaError_t launch_rows_pad(const LaunchArgs& a, cudaStream_t s) {
+  constexpr int N = NR + 4;
+  static_assert(NR % 8 == 4, "padding to the next multiple of 8");
+  static const int mode = [] {
+    const char* e = std::getenv("LAGEN_ROWS_MODE");
+    return e ? std::atoi(e) : cr::default_mode(N, 8);
+  }();
+  static const int wg = [] {
+    const char* e = std::getenv("LAGEN_ROWS_WG");
+    return e ? std::atoi(e) : cr::rows_wg(N, 8);
+  }();
+  if (wg == 1) return launch_rows_wg<N, 8, 1, NR>(a, s, mode);
+  if (wg == 2) return launch_rows_wg<N, 8, 2, NR>(a, s, mode);
+  return launch_rows_wg<N, 8, 4, NR>(a, s, mode);
+}
+
+#define LAGEN_ROWS_PAD_ENTRY(NR) \
+  { NR, 4, 1, (int)cr::RPolicy<NR + 4, 2>::SMEM, &launch_rows_pad<NR> }
 
 #define LAGEN_ROWS_ENTRY(N, B) \
   { N, B, 1, (int)cr::RPolicy<N, 2>::SMEM, &launch_rows<N, B> }

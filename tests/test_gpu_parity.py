@@ -57,7 +57,7 @@ def test_golden_reference_vectors(eq):
         groups.setdefault((e["n"], e["variant"], e["b"]), []).append(e)
     from paper_1906_08613_b200 import _lib
     for (n, v, b), es in groups.items():
-      for engine in ("generic", "warp", "column", "dataflow", "rows", "wave"):
+      for engine in ("generic", "warp", "column", "dataflow", "rows", "wave", "rowspad"):
         if not _lib.engine_supported(EQ_CODES[eq], n, b, v, engine):
             continue
         ins = [np.stack([d[f"in_{e['case']}_{n}_{nm}"] for e in es]) for nm in EQ_INPUTS[eq]]
@@ -89,7 +89,7 @@ def test_every_variant_vs_oracle(eq, n, oracle_mod):
     assert (ref_info == 0).all()
     res_tol = 10 * n * EPS
     from paper_1906_08613_b200 import _lib
-    runs = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows", "wave") for v in vs for b in default_blocks(n)
+    runs = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows", "wave", "rowspad") for v in vs for b in default_blocks(n)
             if _lib.engine_supported(EQ_CODES[eq], n, b, v.index, e)]
     for v, b, engine in runs:
         if True:
@@ -132,7 +132,7 @@ def test_non_spd_and_nan_are_reported():
         with pytest.raises(errors.VerificationError):
             executor.solve("cholesky", [A], variant=2, b=4)
         for v in (1, 2):
-            for engine in ("generic", "warp", "column", "dataflow", "rows"):
+            for engine in ("generic", "warp", "column", "dataflow", "rows", "rowspad"):
                 if not _lib.engine_supported(0, n, 4, v, engine):
                     continue
                 X, info = executor.solve("cholesky", [A], variant=v, b=4, check=False, engine=engine)

@@ -57,7 +57,7 @@ def main():
             rows = []
             ref_X = None
             from paper_1906_08613_b200 import _lib
-            cands = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows", "wave")
+            cands = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows", "wave", "rowspad")
                      for v in builtin_variants(eq) for b in default_blocks(n)
                      if _lib.engine_supported(_lib_eq(eq), n, b, v.index, e)]
             if args.engines != "all":
