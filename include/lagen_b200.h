@@ -128,8 +128,9 @@ int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b
 /* Lyapunov v5 / Sylvester v13: 8x8-tile anti-diagonal wavefront, DMMA
  * tile updates with register-resident accumulators (wave.cuh) */
 #define LAGEN_ENGINE_WAVE 6
-/* Cholesky v1 at n = 4 (mod 8): the rows engine's b = 8 kernel of size n + 4
- * on the identity-padded problem (only the real n x n entries move) */
+/* Cholesky v1: the rows engine's b = 8 kernel of a larger size on the
+ * identity-padded problem (n = 4 mod 8 -> n + 4; 104 -> 112; 120 -> 128;
+ * only the real n x n entries move) */
 #define LAGEN_ENGINE_ROWS_PAD 7
 int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
                               long long batch, const double* const* inputs, double* X,

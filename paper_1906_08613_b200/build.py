@@ -76,7 +76,7 @@ def build(force=False, verbose=False, jobs=None):
 
     def compile_one(item):
         src, obj = item
-        cmd = [cc, *ARCH, *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-MD", "-MF", str(obj.with_suffix(".d")),
+        cmd = [cc, *ARCH, *NVCC_FLAGS, *os.environ.get("LAGEN_NVCC_EXTRA", "").split(), f"-I{INCLUDE}", f"-I{CSRC}", "-MD", "-MF", str(obj.with_suffix(".d")),
                "-c", str(src), "-o", str(obj)]
         proc = subprocess.run(cmd, capture_output=True, text=True)
         if proc.returncode != 0:

@@ -25,6 +25,10 @@
 #pragma once
 #include "engine.cuh"
 
+#ifndef LAGEN_ROWS_DBMIN
+#define LAGEN_ROWS_DBMIN 6  // double-buffer (prefetch the next problem) when >= this many slots fit twice
+#endif
+
 namespace lagen {
 namespace cr {
 
@@ -46,7 +50,8 @@ struct RPolicy {
   static constexpr int WG = WG_;
   static constexpr int S1 = BUDGET / (SLOT * 8 + 640);
   static constexpr int S2 = BUDGET / (2 * SLOT * 8 + 640);
-  static constexpr int DB = S2 >= 6 ? 2 : 1;
+  // n <= 48: more problems in flight beats prefetching (measured, profiles/r01_rows_db.txt)
+  static constexpr int DB = (S2 >= LAGEN_ROWS_DBMIN && N > 48) ? 2 : 1;
   static constexpr int P0 = DB == 2 ? S2 : (S1 < 1 ? 1 : S1);
   static constexpr int PMAX = 32 / WG > 16 ? 16 : 32 / WG;  // <= 32 warps per CTA
   static constexpr int P = P0 > PMAX ? PMAX : P0;

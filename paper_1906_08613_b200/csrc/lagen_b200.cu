@@ -74,9 +74,10 @@ const RowsEntry* find_rows(int eq, int n, int b, int variant) {
   return nullptr;
 }
 
-// padded rows engine: Cholesky v1, n = 4 (mod 8), as the b = 8 kernel of n + 4
+// padded rows engine: Cholesky v1 as the b = 8 kernel of a larger size on the
+// identity-padded problem (n = 4 mod 8 -> n + 4; 104 -> 112, 120 -> 128)
 const RowsEntry* find_rows_pad(int eq, int n, int b, int variant) {
-  if (eq != 0 || variant != 1 || b != 4) return nullptr;
+  if (eq != 0 || variant != 1 || (b != 4 && b != 8)) return nullptr;
   for (int p = 0; p < kRowsPadParts; ++p) {
     const RowsPadTable& t = kRowsPadTables[p];
     for (int i = 0; i < *t.n; ++i)

@@ -67,10 +67,9 @@ cudaError_t launch_rows(const LaunchArgs& a, cudaStream_t s) {
 // problem (diag(A, I) = diag(X, I)^T diag(X, I), exact), reading and writing
 // only the real n x n entries — the b = 8 schedule is the faster one
 // (half the iterations of b = 4) at every measured size
-template <int NR>
+template <int NR, int N = NR + 4>
 cudaError_t launch_rows_pad(const LaunchArgs& a, cudaStream_t s) {
-  constexpr int N = NR + 4;
-  static_assert(NR % 8 == 4, "padding to the next multiple of 8");
+  static_assert(N > NR && N % 8 == 0 && NR % 4 == 0, "padding to a multiple of 8");
   static const int mode = [] {
     const char* e = std::getenv("LAGEN_ROWS_MODE");
     return e ? std::atoi(e) : cr::default_mode(N, 8);
@@ -84,8 +83,8 @@ cudaError_t launch_rows_pad(const LaunchArgs& a, cudaStream_t s) {
   return launch_rows_wg<N, 8, 4, NR>(a, s, mode);
 }
 
-#define LAGEN_ROWS_PAD_ENTRY(NR) \
-  { NR, 4, 1, (int)cr::RPolicy<NR + 4, 2>::SMEM, &launch_rows_pad<NR> }
+#define LAGEN_ROWS_PAD_ENTRY(NR, NP) \
+  { NR, 4, 1, (int)cr::RPolicy<NP, 2>::SMEM, &launch_rows_pad<NR, NP> }
 
 #define LAGEN_ROWS_ENTRY(N, B) \
   { N, B, 1, (int)cr::RPolicy<N, 2>::SMEM, &launch_rows<N, B> }
