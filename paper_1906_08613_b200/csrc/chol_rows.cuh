@@ -25,8 +25,15 @@
 #pragma once
 #include "engine.cuh"
 
+// Residency (measured over the sweep, profiles/r01_rows_db.txt): single
+// buffering with up to 16 warps per CTA beats double buffering (prefetch of
+// the next problem) at every n — more problems in flight hide more latency
+// than the prefetch does; 32 warps per CTA spill registers.
+#ifndef LAGEN_ROWS_MAXW
+#define LAGEN_ROWS_MAXW 16
+#endif
 #ifndef LAGEN_ROWS_DBMIN
-#define LAGEN_ROWS_DBMIN 6  // double-buffer (prefetch the next problem) when >= this many slots fit twice
+#define LAGEN_ROWS_DBMIN 1000  // double-buffer when >= this many slots fit twice (off)
 #endif
 
 namespace lagen {
@@ -50,10 +57,9 @@ struct RPolicy {
   static constexpr int WG = WG_;
   static constexpr int S1 = BUDGET / (SLOT * 8 + 640);
   static constexpr int S2 = BUDGET / (2 * SLOT * 8 + 640);
-  // n <= 48: more problems in flight beats prefetching (measured, profiles/r01_rows_db.txt)
-  static constexpr int DB = (S2 >= LAGEN_ROWS_DBMIN && N > 48) ? 2 : 1;
+  static constexpr int DB = S2 >= LAGEN_ROWS_DBMIN ? 2 : 1;
   static constexpr int P0 = DB == 2 ? S2 : (S1 < 1 ? 1 : S1);
-  static constexpr int PMAX = 32 / WG > 16 ? 16 : 32 / WG;  // <= 32 warps per CTA
+  static constexpr int PMAX = LAGEN_ROWS_MAXW / WG > 16 ? 16 : LAGEN_ROWS_MAXW / WG;  // warps per CTA cap
   static constexpr int P = P0 > PMAX ? PMAX : P0;
   static constexpr int WARPS = P * WG;
   static constexpr int RSB = 16 + 64;
