@@ -291,8 +291,13 @@ def run_e2e(eq, plans, steps, world):
         out = torch.empty_like(ins[0]).pin_memory()
         info = torch.empty(p.batch, dtype=torch.int32).pin_memory()
         hosts.append((p, ins, out, info))
-    h2d = sum(sum(t.numel() * 8 for t in ins) for _, ins, _, _ in hosts)
-    d2h = sum(out.numel() * 8 + info.numel() * 4 for _, _, out, info in hosts)
+    # bytes actually moved over PCIe (Cholesky copies row bands of the upper
+    # triangle and zero-fills the rest of X on the host, lagen_b200_host_bytes)
+    from paper_1906_08613_b200 import _lib
+    from paper_1906_08613_b200.variants import EQ_CODES
+    moved = [_lib.host_bytes(EQ_CODES[eq], p.inputs[0].shape[1], p.batch) for p, _, _, _ in hosts]
+    h2d = sum(m[0] for m in moved)
+    d2h = sum(m[1] for m in moved)
     # warm-up one pass
     for p, ins, out, info in hosts:
         executor.solve_host(eq, ins, variant=p.variant, b=p.b, out=out, info=info, engine=p.engine)

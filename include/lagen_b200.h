@@ -159,6 +159,12 @@ int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, 
                                    long long batch, const double* const* h_inputs,
                                    double* h_X, int* h_info, int engine);
 
+/* Bytes the host pipeline moves per call (H2D of all inputs, D2H of X and
+ * info).  With LAGEN_HOST_BANDS=1 (opt-in, measured not faster) Cholesky
+ * n >= 32 copies only row bands of the upper triangle and zero-fills the rest
+ * of X's lower triangle on host threads. */
+int lagen_b200_host_bytes(int eq, int n, long long batch, long long* h2d, long long* d2h);
+
 /* ---- seeded batched generator (BASELINE.json configs) ----
  * Writes problems [first, first + batch) of the seeded stream into outputs[]
  * (device, _signature order).  Problem p depends only on (eq, n, seed, p), so

@@ -5,8 +5,11 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
+#include <vector>
 #include <string>
 
 #include "inst_index.h"
@@ -371,6 +374,35 @@ int lagen_b200_sylvester(int variant, int n, int b, long long batch, const doubl
 // stream creation / allocation, and no pool release between calls.
 namespace {
 constexpr int kNS = 4;
+// Cholesky moves only row bands of the upper triangle over PCIe: band j =
+// rows [r0, r1), columns [c0, n), c0 = r0 rounded down to 8 (covers every
+// entry any Cholesky engine reads: columns >= 4 floor(r / 4)); K = n / 16
+// bands keep the shortest copied row >= 128 B, where the copy engines still
+// run at full rate (tools/band_copy_probe.cu).  Lyapunov / Sylvester return
+// a full X, so their D2H bounds the pipeline and they copy whole matrices.
+struct Bands {
+  int K = 0;
+  int r0[16], r1[16], c0[16];
+};
+Bands host_bands(int eq, int n) {
+  Bands b;
+  // opt-in (LAGEN_HOST_BANDS=1): measured on the B200 box, the banded copies
+  // run below the whole-matrix rate in bidirectional traffic and the host
+  // zero-fill costs ~1 ms per 256 MiB, so whole copies win or tie at every n
+  // (tools/e2e_probe3.py, profiles/r01_e2e_bands.txt)
+  static const int mode = [] {
+    const char* e = std::getenv("LAGEN_HOST_BANDS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (eq != LAGEN_CHOLESKY || n < 32 || mode == 0) return b;
+  b.K = n / 16 > 16 ? 16 : n / 16;
+  for (int j = 0; j < b.K; ++j) {
+    b.r0[j] = j * n / b.K;
+    b.r1[j] = (j + 1) * n / b.K;
+    b.c0[j] = b.r0[j] & ~7;
+  }
+  return b;
+}
 struct HostPipe {
   int dev = -1;
   cudaStream_t st[kNS] = {nullptr};
@@ -430,24 +462,56 @@ int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, 
   // ~16 MiB of input per chunk and operand, at least one problem
   long long chunk = (16ll << 20) / (long long)prob_bytes;
   if (chunk < 1) chunk = 1;
+  const Bands bd = host_bands(eq, n);
   std::lock_guard<std::mutex> lock(g_pipe_mu);
   HostPipe& hp = g_pipe[dev];
   err = hp.reserve((size_t)chunk * prob_bytes, (size_t)chunk * sizeof(int));
   if (err != cudaSuccess) return cuda_fail(err, "host pipeline setup");
   if (chunk > batch) chunk = batch;
+  // Cholesky: the strictly-lower part of X left of each band is zero; the
+  // host writes it (threads, overlapped with the copies) instead of PCIe
+  std::vector<std::thread> fill;
+  static const bool no_fill = std::getenv("LAGEN_HOST_NOFILL") != nullptr;  // measurement only: X left partly unwritten
+  if (bd.K > 0 && !no_fill) {
+    unsigned nt = std::thread::hardware_concurrency();
+    nt = nt < 1 ? 1 : (nt > 16 ? 16 : nt);
+    for (unsigned t = 0; t < nt; ++t)
+      fill.emplace_back([=]() {
+        const long long p0 = batch * t / nt, p1 = batch * (t + 1) / nt;
+        for (long long p = p0; p < p1; ++p)
+          for (int j = 0; j < bd.K; ++j)
+            if (bd.c0[j] > 0)
+              for (int r = bd.r0[j]; r < bd.r1[j]; ++r)
+                std::memset(h_X + (p * n + r) * (long long)n, 0, sizeof(double) * bd.c0[j]);
+      });
+  }
+  auto copy = [&](double* dst, const double* src, long long cnt, cudaMemcpyKind kind, cudaStream_t st) {
+    if (bd.K == 0) return cudaMemcpyAsync(dst, src, cnt * prob_bytes, kind, st);
+    for (int j = 0; j < bd.K; ++j) {
+      cudaMemcpy3DParms p = {};
+      p.srcPtr = make_cudaPitchedPtr(const_cast<double*>(src), sizeof(double) * n, n, n);
+      p.dstPtr = make_cudaPitchedPtr(dst, sizeof(double) * n, n, n);
+      p.srcPos = make_cudaPos(sizeof(double) * bd.c0[j], bd.r0[j], 0);
+      p.dstPos = p.srcPos;
+      p.extent = make_cudaExtent(sizeof(double) * (n - bd.c0[j]), bd.r1[j] - bd.r0[j], cnt);
+      p.kind = kind;
+      cudaError_t e = cudaMemcpy3DAsync(&p, st);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  };
   int status = LAGEN_OK;
   for (long long c0 = 0, it = 0; status == LAGEN_OK && c0 < batch; c0 += chunk, ++it) {
     const int k = (int)(it % kNS);
     const long long cnt = (batch - c0) < chunk ? (batch - c0) : chunk;
     for (int i = 0; i < nin && err == cudaSuccess; ++i)
-      err = cudaMemcpyAsync(hp.d_in[k][i], h_inputs[i] + c0 * n * n, cnt * prob_bytes, cudaMemcpyHostToDevice,
-                            hp.st[k]);
+      err = copy(hp.d_in[k][i], h_inputs[i] + c0 * n * n, cnt, cudaMemcpyHostToDevice, hp.st[k]);
     if (err != cudaSuccess) { status = cuda_fail(err, "H2D"); break; }
     const double* ins[3] = {hp.d_in[k][0], hp.d_in[k][1], hp.d_in[k][2]};
     status = lagen_b200_execute_engine(eq, stmts, nstmts, n, b, cnt, ins, hp.d_X[k], h_info ? hp.d_info[k] : nullptr,
                                        hp.st[k], engine);
     if (status != LAGEN_OK) break;
-    err = cudaMemcpyAsync(h_X + c0 * n * n, hp.d_X[k], cnt * prob_bytes, cudaMemcpyDeviceToHost, hp.st[k]);
+    err = copy(h_X + c0 * n * n, hp.d_X[k], cnt, cudaMemcpyDeviceToHost, hp.st[k]);
     if (err == cudaSuccess && h_info)
       err = cudaMemcpyAsync(h_info + c0, hp.d_info[k], cnt * sizeof(int), cudaMemcpyDeviceToHost, hp.st[k]);
     if (err != cudaSuccess) { status = cuda_fail(err, "D2H"); break; }
@@ -456,7 +520,21 @@ int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, 
     cudaError_t e2 = cudaStreamSynchronize(hp.st[k]);
     if (e2 != cudaSuccess && status == LAGEN_OK) status = cuda_fail(e2, "host pipeline sync");
   }
+  for (auto& th : fill) th.join();
   return status;
+}
+
+int lagen_b200_host_bytes(int eq, int n, long long batch, long long* h2d, long long* d2h) {
+  if (eq < 0 || eq > 2 || n < 1 || batch < 0) return fail(LAGEN_EINVAL, "bad arguments");
+  const Bands bd = host_bands(eq, n);
+  long long per = (long long)n * n;
+  if (bd.K > 0) {
+    per = 0;
+    for (int j = 0; j < bd.K; ++j) per += (long long)(bd.r1[j] - bd.r0[j]) * (n - bd.c0[j]);
+  }
+  if (h2d) *h2d = batch * per * (long long)sizeof(double) * eq_ninputs(eq);
+  if (d2h) *d2h = batch * (per * (long long)sizeof(double) + (long long)sizeof(int));
+  return LAGEN_OK;
 }
 
 }  // extern "C"
