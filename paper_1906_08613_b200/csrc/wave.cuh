@@ -39,6 +39,13 @@
 
 #include "engine.cuh"
 
+// L2 prefetch of the next problem's whole operands (cp.async.bulk.prefetch):
+// measured off — it read the unused triangles too and the prefetched lines
+// were partly evicted before use (DRAM traffic 1.4-2.1x the compulsory bytes),
+// without a speed-up (profiles/r01_wave_traffic.txt)
+#ifndef WAVE_PREFETCH
+#define WAVE_PREFETCH 0
+#endif
 #ifndef WAVE_SOLVE
 #define WAVE_SOLVE 1
 #endif
@@ -195,7 +202,7 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
     if (rank == 0) {
       *flag = 0;
       const long long nxt = prob + stride;
-      if (nxt < batch) {  // next problem's operands -> L2 while this one runs
+      if (WAVE_PREFETCH && nxt < batch) {  // next problem's operands -> L2 while this one runs
         const unsigned bytes = (unsigned)(NN * 8);
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Lg + nxt * NN), "r"(bytes) : "memory");
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Cg + nxt * NN), "r"(bytes) : "memory");
