@@ -410,7 +410,16 @@ def summarize(eq, res, steps, peaks, world):
                 "unit": "TFLOP/s", "frac": round(achieved_tf / peaks["fp64_tflops"], 4)}
     t_roof_nom = sum(r["batch"] * 0 + r["ms"] * r["roofline_frac_nominal"] for r in res["per_n"]) * 1e-3
     roof["frac_of_nominal_roofline"] = round(t_roof_nom / t_kernels, 4)
+    # DRAM bytes per launch of the profiled kernel (ncu --set full), against
+    # its algorithmic bytes: profiles/r01_traffic.json, written from the
+    # committed ncu captures (the box has no ncu in the timed run)
     roof["traffic"] = None
+    tf = REPO / "profiles" / "r01_traffic.json"
+    if tf.exists():
+        t = json.loads(tf.read_text()).get(eq)
+        if t:
+            roof["traffic"] = t["dram_bytes_per_launch"]
+            roof["traffic_kernel"] = {k: t[k] for k in ("kernel", "algorithmic_bytes_per_launch", "ratio", "source")}
     return value, ms, roof
 
 
