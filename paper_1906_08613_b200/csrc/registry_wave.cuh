@@ -19,7 +19,7 @@ struct WaveEntry {
 
 // default geometry: enough warps that a diagonal spreads over <= 4 groups per
 // warp and <= ~32 accumulator tiles per warp; then as many problems per CTA as
-// registers (~4 S + 112 per thread, spill-free at that cap) and shared memory allow
+// registers (~4 S + 136 per thread, spill-free at that cap) and shared memory allow
 template <int EQ, int N>
 struct WCfg {
   static constexpr int T = (N + 7) / 8;
@@ -27,13 +27,27 @@ struct WCfg {
   static constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
   static constexpr int mx(int a, int b) { return a > b ? a : b; }
   static constexpr int mn(int a, int b) { return a < b ? a : b; }
-  static constexpr int NW = mx(mx(cdiv(T, 4), cdiv(NT, 32)), 1);
+  // measured: ~136 registers per thread beside the accumulators (spill-free)
+  static constexpr int regs(int nw) { return mn(255, 4 * cdiv(NT, nw) + 136); }
+  static constexpr int slotb(int nw) {
+    return 8 * (T * (T + 1) / 2 * (EQ == 2 ? 2 : 1) * 64 + 2 * T * 68 + T * 80 + nw * 4 * 72 + 2);
+  }
+  static constexpr int pp(int nw) {
+    return mx(1, mn(mn(65536 / (regs(nw) * 32 * nw), (227 * 1024) / slotb(nw)), mn(32 / nw, nw == 1 ? 32 : 15)));
+  }
+  // enough warps that a diagonal spreads over <= 4 groups per warp and
+  // <= ~32 accumulator tiles per warp; then, while fewer than 8 warps per SM
+  // are resident, one more warp per problem (more solves in parallel, more
+  // latency hidden) as long as the registers allow
+  static constexpr int nw_pick() {
+    int nw = mx(mx(cdiv(T, 4), cdiv(NT, 32)), 1);
+    while (pp(nw) * nw < 8 && nw < T && regs(nw + 1) * 32 * (nw + 1) <= 65536) ++nw;
+    return nw;
+  }
+  static constexpr int NW = nw_pick();
   static constexpr int S = wave::WPol<EQ, N, NW, 1>::S;
-  static constexpr int REGS = mn(255, 4 * S + 112);  // measured: ~112 beside the accumulators
-  static constexpr int PPR = 65536 / (REGS * 32 * NW);
-  static constexpr int SLOTB = (int)(wave::WPol<EQ, N, NW, 1>::SLOT * 8);
-  static constexpr int PPS = (227 * 1024) / SLOTB;
-  static constexpr int PP = mx(1, mn(mn(PPR, PPS), mn(32 / NW, NW == 1 ? 32 : 15)));
+  static constexpr int PP = pp(NW);
+  static_assert(slotb(NW) == (int)(wave::WPol<EQ, N, NW, 1>::SLOT * 8), "slot size model");
 };
 
 template <int EQ, int N, int NW, int PP>

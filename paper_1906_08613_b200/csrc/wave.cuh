@@ -318,24 +318,50 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
           y[s] = yload(s);
           h[s] = 0.0;
         }
-        double uc[8];
+        // setup with independent loads issued first (the compiler must keep a
+        // shared load after any earlier shared store, so load -> compute ->
+        // store order is explicit; divergent selects instead of branches)
+        double uc[8], dg[8];
         uc[0] = 0.0;
 #pragma unroll
-        for (int j = 1; j < 8; ++j) uc[j] = j <= c ? uat(c - j) : 0.0;
+        for (int j = 1; j < 8; ++j) uc[j] = uat(c >= j ? c - j : 0);
         const double ucc = uat(c);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) scr[r] = recip(Ld[sw(r, r)] + ucc);
+        for (int r = 0; r < 8; ++r) dg[r] = Ld[sw(r, r)];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) uc[j] = j <= c ? uc[j] : 0.0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) dg[r] = recip(dg[r] + ucc);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) scr[r] = dg[r];
         __syncwarp();
+        // per-step coefficients (pivot reciprocal, column r of L_II below the
+        // diagonal), loaded one step ahead so no load waits behind a store
+        struct Co {
+          double piv;
+          double2 a, b, cc, d;
+        };
+        auto coload = [&](int s) -> Co {
+          const int r = s - c;
+          const int rc = r < 0 ? 0 : (r > 7 ? 7 : r);
+          const double2* lc = reinterpret_cast<const double2*>(Ls + 10 * rc);
+          Co o;
+          o.piv = (r >= 0 && r < 8) ? scr[rc] : 0.0;
+          o.a = lc[0];
+          o.b = lc[1];
+          o.cc = lc[2];
+          o.d = lc[3];
+          return o;
+        };
+        Co cur = coload(0);
         // one wavefront step; the dependence on the previous step is kept to
         // shfl(x(r, c-1)) -> FMA -> MUL and push(x(r-1, c)) -> ADD -> FMA -> MUL:
         // contributions of values >= 2 steps old are summed off that chain
         auto step = [&](int s, int u) {
           const int r = s - c;
           const bool act = r >= 0 && r < 8;
-          const int rc = r < 0 ? 0 : (r > 7 ? 7 : r);
-          const double piv = act ? scr[rc] : 0.0;
-          const double2* lc = reinterpret_cast<const double2*>(Ls + 10 * rc);
-          const double2 l01 = lc[0], l23 = lc[1], l45 = lc[2], l67 = lc[3];
+          const Co nxt = coload(s + 1 <= 14 ? s + 1 : 14);
+          const double ynew = yload(s + 8);
           // row contributions: x(r, c - j) from lane c - j, computed j steps ago
           double t0 = 0.0, t1 = 0.0;
 #pragma unroll
@@ -348,14 +374,15 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
           const double x1 = __shfl_sync(0xffffffffu, h[(u - 1) & 7], (lane & ~7) | (c >= 1 ? c - 1 : c));
           double v = y[u] - (t0 + t1);
           v = fma(-x1, uc[1], v);
-          const double x = v * piv;
+          const double x = v * cur.piv;
           h[u] = x;
           // own column: rows r + e take L(r + e, r) x (row r + 1 first: next step)
-          const double coef[8] = {0.0, l01.y, l23.x, l23.y, l45.x, l45.y, l67.x, l67.y};
+          const double coef[8] = {0.0, cur.a.y, cur.b.x, cur.b.y, cur.cc.x, cur.cc.y, cur.d.x, cur.d.y};
 #pragma unroll
           for (int e = 1; e < 8; ++e) y[(u + e) & 7] = fma(-coef[e], x, y[(u + e) & 7]);
-          y[u] = yload(s + 8);
+          y[u] = ynew;
           if (act && live) Pt[sw(r, c)] = -x;
+          cur = nxt;
         };
 #pragma unroll
         for (int u = 0; u < 8; ++u) step(u, u);
