@@ -102,14 +102,33 @@ struct KRow {
 // (A_pad = diag(A, I) -> X_pad = diag(X, I), exactly)
 template <int N, int G, int NR = N>
 __device__ __forceinline__ void load_rows(double* xs, const double* __restrict__ src, int rank) {
+  // warps over rows, lanes over the row's 16-byte pairs from its first stored
+  // column: no per-element division and no iterations over the lower part
+  // (when a row's pair count is not a multiple of 32 above 32, the flattened
+  // loop keeps every lane busy instead)
   constexpr int H = N / 2;
-  for (int u = rank; u < N * H; u += G) {
-    const int r = u / H, c = 2 * (u - r * H);
-    if (c >= 4 * (r >> 2)) {
-      if (NR == N || (r < NR && c < NR))
-        cp_async16(xs + Rows<N>::at(r, c), src + r * NR + c);
-      else
-        *reinterpret_cast<double2*>(xs + Rows<N>::at(r, c)) = make_double2(r == c ? 1.0 : 0.0, r == c + 1 ? 1.0 : 0.0);
+  if constexpr (H <= 32 || H % 32 == 0) {
+    constexpr int NWG = G / 32;
+    const int w = rank >> 5, lane = rank & 31;
+    for (int r = w; r < N; r += NWG) {
+      const int c0 = 4 * (r >> 2);
+      double* row = xs + Rows<N>::off(r) - c0;
+      for (int c = c0 + 2 * lane; c < N; c += 64) {
+        if (NR == N || (r < NR && c < NR))
+          cp_async16(row + c, src + r * NR + c);
+        else
+          *reinterpret_cast<double2*>(row + c) = make_double2(r == c ? 1.0 : 0.0, r == c + 1 ? 1.0 : 0.0);
+      }
+    }
+  } else {
+    for (int u = rank; u < N * H; u += G) {
+      const int r = u / H, c = 2 * (u - r * H);
+      if (c >= 4 * (r >> 2)) {
+        if (NR == N || (r < NR && c < NR))
+          cp_async16(xs + Rows<N>::at(r, c), src + r * NR + c);
+        else
+          *reinterpret_cast<double2*>(xs + Rows<N>::at(r, c)) = make_double2(r == c ? 1.0 : 0.0, r == c + 1 ? 1.0 : 0.0);
+      }
     }
   }
 }
@@ -363,13 +382,28 @@ __device__ __forceinline__ void trsm(double* xs, int r0, const double* rsb, int 
 // block row [r0, r0 + B) -> X (row-major, zeros left of the diagonal)
 template <int N, int B, int NR = N>
 __device__ __forceinline__ void store_rows(double* __restrict__ dst, const double* xs, int r0, int rank, int nthr) {
-  constexpr int H = NR / 2;  // 16-byte units per (real) row
+  // warps over the block row's rows, lanes over 16-byte pairs (coalesced)
   const int nb = r0 + B <= NR ? B : NR - r0;  // real rows of this block row
-  for (int u = rank; u < nb * H; u += nthr) {
-    const int i = u / H, r = r0 + i, c = 2 * (u - i * H);
-    double2 v = make_double2(0.0, 0.0);
-    if (c >= 4 * (r >> 2)) v = *reinterpret_cast<const double2*>(xs + Rows<N>::at(r, c));
-    __stcs(reinterpret_cast<double2*>(dst + r * NR + c), v);
+  constexpr int H = NR / 2;
+  if constexpr (H <= 32 || H % 32 == 0) {
+    const int w = rank >> 5, nw = nthr >> 5, lane = rank & 31;
+    for (int i = w; i < nb; i += nw) {
+      const int r = r0 + i, c0 = 4 * (r >> 2);
+      const double* row = xs + Rows<N>::off(r) - c0;
+      double* drow = dst + r * NR;
+      for (int c = 2 * lane; c < NR; c += 64) {
+        double2 v = make_double2(0.0, 0.0);
+        if (c >= c0) v = *reinterpret_cast<const double2*>(row + c);
+        __stcs(reinterpret_cast<double2*>(drow + c), v);
+      }
+    }
+  } else {
+    for (int u = rank; u < nb * H; u += nthr) {
+      const int i = u / H, r = r0 + i, c = 2 * (u - i * H);
+      double2 v = make_double2(0.0, 0.0);
+      if (c >= 4 * (r >> 2)) v = *reinterpret_cast<const double2*>(xs + Rows<N>::at(r, c));
+      __stcs(reinterpret_cast<double2*>(dst + r * NR + c), v);
+    }
   }
 }
 
