@@ -33,7 +33,11 @@ def main():
            "`" + tag + "_ncu_launches_chol_sweep.csv` (ncu launch list, `--metrics gpu__time_duration.sum "
            "--clock-control none`), `" + tag + "_ncu_full_*.csv` (`ncu --set full` of top kernels), "
            "`fp64_peaks.json` / `fp64_latency.json` (tools/fp64_peaks.cu, tools/fp64_latency.cu), "
-           "`" + tag + "_rows_modes.txt` (rows-engine work-split sweep), `" + tag + "_phase_profile.txt`.", "",
+           "`" + tag + "_rows_modes.txt` (rows-engine work-split sweep), `" + tag + "_phase_profile.txt`, "
+           "`" + tag + "_ncu_launches_sweeps.md` (per-launch time and DRAM bytes of one step of each sweep), "
+           "`" + tag + "_ncu_full_top_kernels.csv` (ncu --set full metrics of the top kernels), "
+           "`" + tag + "_traffic.json`, `" + tag + "_wave_traffic.txt`, `" + tag + "_rows_db.txt`, "
+           "`" + tag + "_e2e_bands.txt`.", "",
            "## Peaks used", "",
            f"- HBM: {b['peaks']['hbm_gbs']} GB/s ({b['peaks']['source']['hbm_gbs']}).",
            f"- FP64: {b['peaks']['fp64_tflops']} TFLOP/s ({b['peaks']['source']['fp64_tflops']}).", ""]
