@@ -438,8 +438,8 @@ __global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)
   const int warp = threadIdx.x >> 5, lane = lane_id();
   Grp gr;
   gr.id = warp / WG;
-  gr.wig = warp % WG;
-  gr.rank = threadIdx.x % G;
+  gr.wig = (warp % WG + WG - eng::lead_warp(gr.id, WG)) % WG;  // 0: the leaf warp
+  gr.rank = gr.wig * 32 + lane;
   gr.rsb = rsb_all + P::RSB * gr.id;
   gr.scr = P::SCR ? scr_all + (size_t)P::SCR * gr.id : nullptr;
   gr.prof = nullptr;

@@ -138,6 +138,15 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// In-group index of the warp that carries a problem group's serial chain
+// (CHOL leaf): groups of WG consecutive warps would otherwise put every
+// group's leaf warp on the same SM sub-partition (warp % 4), where the
+// leaves' FP64 / MUFU work queues behind each other; this picks a distinct
+// sub-partition per group where the group size allows.
+__host__ __device__ constexpr int lead_warp(int g, int WG) {
+  return WG == 4 ? g % 4 : WG == 2 ? (g / 2) % 2 : WG == 3 ? (2 * g) % 4 : 0;
+}
+
 // A problem is owned by a group of WG warps (G = 32 * WG threads).
 struct Grp {
   int rank;     // 0 .. G-1
