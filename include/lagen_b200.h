@@ -104,7 +104,13 @@ int lagen_b200_sylvester(int variant, int n, int b, long long batch,
                          double* X, int* info, void* stream);
 
 /* ---- generic executor: interpret_algorithm(alg, inst, b), verify.py:221 ----
- * inputs[] in _signature order: chol {A}, lyap {L, S}, sylv {L, U, C}. */
+ * inputs[] in _signature order: chol {A}, lyap {L, S}, sylv {L, U, C}.
+ * Any 1 <= n <= 128 with b dividing n (the reference's own condition,
+ * verify.py:232-233): (n, b) without a compiled instance (n not a multiple of
+ * 4, or e.g. b = 1) runs as the identity-padded problem of the next multiple
+ * of 4 with that size's block size (exact: diag(A, I) -> diag(X, I); zero
+ * right-hand-side rows / columns -> zero X rows / columns), through a
+ * stream-ordered scratch allocation of (#inputs + 1) padded batches. */
 int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
                        long long batch, const double* const* inputs, double* X,
                        int* info, void* stream);

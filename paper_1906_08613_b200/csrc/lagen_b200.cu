@@ -187,14 +187,65 @@ int validate(int eq, const lagen_stmt* stmts, int nstmts) {
   return LAGEN_OK;
 }
 
+// Sizes without a compiled instance (n not a multiple of 4, or a block size
+// the instances do not use, e.g. (7, 7) or (10, 5)) run as the identity-padded
+// problem of the next multiple of 4 — exact for all three equations:
+//   A_p = diag(A, I)                  ->  X_p = diag(X, I)     (Cholesky)
+//   L_p = diag(L, I), S_p = [S 0; 0 0] ->  X_p = [X 0; 0 0]     (Lyapunov)
+//   L_p = diag(L, I), U_p = diag(U, I), C_p = [C 0; 0 0] -> X_p = [X 0; 0 0]
+// (the unknown's first n rows / columns never read the padded ones: every
+// variant is a forward recursion over the leading blocks), with the padded
+// size's own block size b' (b itself when it divides n' and has an instance).
+// Returns n' (0: none) and sets *bp.
+int padded_size(int eq, int n, int b, int* bp) {
+  const int np = n < 4 ? 4 : (n + 3) & ~3;
+  if (np > 128) return 0;
+  const int cands[4] = {b, 8, 4, 16};
+  for (int c : cands)
+    if (c >= 1 && np % c == 0 && find_entry(eq, np, c)) {
+      *bp = c;
+      return np;
+    }
+  return 0;
+}
+
 int check_common(int eq, int n, int b, long long batch) {
   if (eq < 0 || eq > 2) return fail(LAGEN_EINVAL, "unknown equation");
   if (batch < 0) return fail(LAGEN_EINVAL, "negative batch");
   if (n < 1 || b < 1 || n % b) return fail(LAGEN_EUNSUPPORTED, "block size does not divide n");
-  if (!find_entry(eq, n, b))
+  int bp = 0;
+  if (!find_entry(eq, n, b) && !padded_size(eq, n, b, &bp))
     return fail(LAGEN_EUNSUPPORTED, "no sm_100a instance for (n=" + std::to_string(n) + ", b=" +
                                         std::to_string(b) + ")");
   return LAGEN_OK;
+}
+
+// problem p, element (r, c) of the n' x n' padded operand
+__global__ void pad_kernel(const double* __restrict__ src, double* __restrict__ dst, long long batch, int n, int np,
+                           double diag) {
+  const long long total = batch * np * np;
+  for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < total;
+       u += (long long)gridDim.x * blockDim.x) {
+    const long long p = u / (np * np);
+    const int e = (int)(u - p * np * np), r = e / np, c = e - r * np;
+    dst[u] = (r < n && c < n) ? src[(p * n + r) * n + c] : (r == c ? diag : 0.0);
+  }
+}
+
+__global__ void unpad_kernel(const double* __restrict__ src, double* __restrict__ dst, long long batch, int n,
+                             int np) {
+  const long long total = batch * n * n;
+  for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < total;
+       u += (long long)gridDim.x * blockDim.x) {
+    const long long p = u / (n * n);
+    const int e = (int)(u - p * n * n), r = e / n, c = e - r * n;
+    dst[u] = src[(p * np + r) * np + c];
+  }
+}
+
+int grid_for(long long total) {
+  long long g = (total + 255) / 256;
+  return (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
 }
 
 const lagen_stmt* builtin(int eq, int variant, int* count) {
@@ -292,6 +343,32 @@ int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int 
   if (!inputs || !X) return fail(LAGEN_EINVAL, "null buffer");
   for (int i = 0; i < eq_ninputs(eq); ++i)
     if (!inputs[i]) return fail(LAGEN_EINVAL, "null input buffer");
+  if (!find_entry(eq, n, b)) {  // identity-padded problem (see padded_size)
+    int bp = 0;
+    const int np = padded_size(eq, n, b, &bp);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int nin = eq_ninputs(eq);
+    const size_t per = (size_t)batch * np * np;
+    double* buf = nullptr;
+    cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(double) * per * (nin + 1), s);
+    if (err != cudaSuccess) return cuda_fail(err, "padded buffers");
+    const double* pin[3] = {nullptr, nullptr, nullptr};
+    // identity on the diagonal of L, U and A; zeros in S and C
+    for (int i = 0; i < nin; ++i) {
+      const bool rhs = (eq == LAGEN_LYAPUNOV && i == 1) || (eq == LAGEN_SYLVESTER && i == 2);
+      pad_kernel<<<grid_for((long long)per), 256, 0, s>>>(inputs[i], buf + per * i, batch, n, np, rhs ? 0.0 : 1.0);
+      pin[i] = buf + per * i;
+    }
+    double* Xp = buf + per * nin;
+    int rc2 = lagen_b200_execute_profile(eq, stmts, nstmts, np, bp, batch, pin, Xp, info, stream, engine, d_prof);
+    if (rc2 == LAGEN_OK) {
+      unpad_kernel<<<grid_for(batch * n * n), 256, 0, s>>>(Xp, X, batch, n, np);
+      err = cudaGetLastError();
+      if (err != cudaSuccess) rc2 = cuda_fail(err, "unpad launch");
+    }
+    cudaFreeAsync(buf, s);
+    return rc2;
+  }
   LaunchArgs a;
   std::memset(&a, 0, sizeof(a));
   std::memcpy(a.sl.s, stmts, sizeof(lagen_stmt) * nstmts);

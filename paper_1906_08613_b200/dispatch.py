@@ -35,5 +35,8 @@ def select(eq_name, n):
     if entry is not None:
         return {"variant": int(entry["variant"]), "b": int(entry["b"]), "source": "autotune",
                 "engine": entry.get("engine", "auto")}
-    blocks = default_blocks(n) or [4]
+    # sizes without an admissible reference block (n not a multiple of 4) run
+    # as the identity-padded problem (lagen_b200.h); b = its largest divisor
+    # of n from (8, 4, 2, 1) keeps the reference's b | n condition
+    blocks = default_blocks(n) or [max(d for d in (8, 4, 2, 1) if n % d == 0)]
     return {"variant": _FALLBACK_VARIANT[eq_name], "b": max(blocks), "source": "fallback"}

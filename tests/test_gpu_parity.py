@@ -106,6 +106,50 @@ def test_every_variant_vs_oracle(eq, n, oracle_mod):
                 assert np.array_equal(X, np.transpose(X, (0, 2, 1)))
 
 
+ODD_N = [1, 2, 3, 5, 6, 7, 9, 10, 13, 18, 30, 31, 33, 47, 63, 66, 97, 127]
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+@pytest.mark.parametrize("n", ODD_N)
+def test_sizes_without_instance_vs_oracle(eq, n, oracle_mod):
+    """n not a multiple of 4 (BASELINE target: every n in 4..128): the
+    identity-padded path of the C ABI against the oracle's own (n, b) run,
+    for every variant, with the reference's admissible b (b | n)."""
+    batch = 32
+    ins_d = executor.generate(eq, n, seed=1000 + n, batch=batch)
+    ins_h = [t.cpu().numpy() for t in ins_d]
+    blocks = sorted({b for b in (1, 2, 4, 8, n) if n % b == 0})
+    res_tol = 10 * max(n, 4) * EPS
+    for v in builtin_variants(eq):
+        for b in blocks:
+            ref_X, ref_info = oracle_mod.execute(eq, v.statements, n, b, ins_h)
+            assert (ref_info == 0).all()
+            X, info = executor.solve(eq, ins_d, variant=v.index, b=b)
+            X = X.cpu().numpy()
+            assert X.shape == (batch, n, n)
+            assert (info.cpu().numpy() == 0).all(), (eq, n, v.index, b)
+            err = rel_diff(X, ref_X).max()
+            assert err <= REL_TOL, (eq, n, v.index, b, err)
+            res = oracle_mod.residual(eq, n, ins_h, X)
+            assert res.max() <= res_tol, (eq, n, v.index, b, res.max() / (n * EPS))
+    # default selection (dispatch fallback b) and the host pipeline agree
+    X0, _ = executor.solve(eq, ins_d)
+    Xh, _ = executor.solve_host(eq, ins_h)
+    assert np.array_equal(np.asarray(Xh), X0.cpu().numpy())
+
+
+def test_padded_sizes_report_non_spd_index():
+    n = 7
+    A = torch.eye(n, dtype=torch.float64, device="cuda").repeat(2, 1, 1)
+    A[1, 5, 5] = -1.0
+    with pytest.raises(errors.VerificationError, match="index 5"):
+        executor.solve("cholesky", [A], variant=1, b=1)
+    _, info = executor.solve("cholesky", [A], variant=1, b=7, check=False)
+    assert info.cpu().tolist() == [0, 6]
+    with pytest.raises(errors.LagenError):
+        executor.solve("cholesky", [A], variant=1, b=2)  # 2 does not divide 7 (verify.py:232-233)
+
+
 def test_known_answers():
     for n in (4, 8, 16, 64):
         I = torch.eye(n, dtype=torch.float64, device="cuda").expand(3, n, n).contiguous()
