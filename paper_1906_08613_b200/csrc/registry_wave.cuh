@@ -9,6 +9,22 @@
 #include "registry.cuh"
 #include "wave.cuh"
 
+// Registers per thread beside the accumulators in the geometry model: sets
+// how many problems share a CTA (PP) and so the register cap per thread.
+// 136 is spill-free for most sizes; where the solve spilled its lane /
+// address state to local memory at that cap, fewer problems per CTA with a
+// spill-free register budget measured faster (A/B over the sweep sizes,
+// profiles/r01_wave_geometry.md) — keyed by the tile count T = ceil(n / 8),
+// which fixes the geometry.  LAGEN_WAVE_REGBASE forces one value (tuning).
+#ifndef LAGEN_WAVE_REGBASE
+#define LAGEN_WAVE_REGBASE 0
+#endif
+constexpr int wave_regbase(int eq, int t) {
+  if (LAGEN_WAVE_REGBASE) return LAGEN_WAVE_REGBASE;
+  if (eq == 2) return (t == 4 || t == 5) ? 170 : 136;                                   // Sylvester
+  return t == 4 ? 200 : (t == 6 || t == 7 || t == 10 || t == 11) ? 170 : 136;           // Lyapunov
+}
+
 namespace lagen {
 
 struct WaveEntry {
@@ -28,7 +44,7 @@ struct WCfg {
   static constexpr int mx(int a, int b) { return a > b ? a : b; }
   static constexpr int mn(int a, int b) { return a < b ? a : b; }
   // measured: ~136 registers per thread beside the accumulators (spill-free)
-  static constexpr int regs(int nw) { return mn(255, 4 * cdiv(NT, nw) + 136); }
+  static constexpr int regs(int nw) { return mn(255, 4 * cdiv(NT, nw) + wave_regbase(EQ, T)); }
   static constexpr int slotb(int nw) {
     return 8 * (T * (T + 1) / 2 * (EQ == 2 ? 2 : 1) * 64 + 2 * T * 68 + T * 80 + nw * 4 * 72 + 2);
   }
