@@ -154,10 +154,15 @@ __device__ __forceinline__ void s1_tile(double* xs, int t0, int ks0, int ks1) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) dmma(c0[u], c1[u], a[u], a[u]);
   }
-  for (int u = 0; ks < ks1; ++ks, ++u) {
-    const double a = xs[kr.p + t0 + ga];
-    kr.step();
-    dmma(c0[u & 3], c1[u & 3], a, a);
+  // remainder (< 4 k-steps) with static accumulator indices: a runtime
+  // index (u & 3) put c0 / c1 in local memory for the whole tile
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    if (ks + u < ks1) {
+      const double a = xs[kr.p + t0 + ga];
+      kr.step();
+      dmma(c0[u], c1[u], a, a);
+    }
   }
   const double x0 = (c0[0] + c0[1]) + (c0[2] + c0[3]);
   const double x1 = (c1[0] + c1[1]) + (c1[2] + c1[3]);
