@@ -420,11 +420,13 @@ __device__ unsigned long long prof_buf[16];
 // launch mode = k-split (1) | work split << 2.  Sweep of WG in {1, 2, 4} x
 // modes {1, 5, 9, 13} over n = 36..128 at full 256 MiB batches
 // (LAGEN_ROWS_WG / LAGEN_ROWS_MODE + tools/engine_compare.py,
-// profiles/r01_rows_wg_modes.txt); sizes below 36 use the column engine.
+// profiles/r01_rows_wg_modes.txt; the b = 8 row re-measured after the leaf
+// warp placement and S1 fixes, profiles/r01_rows_tune.txt, which moved
+// n = 56, 64, 72, 80, 112); sizes below 36 use the column engine.
 constexpr unsigned char kRowsWG[2][33] = {{1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 2, 1, 1, 2, 1, 1, 2, 1, 2, 2, 2, 2, 2, 2, 2, 2, 2, 4, 4, 4},
-                                            {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 1, 2, 1, 1, 1, 1, 1, 2, 1, 2, 1, 2, 1, 2, 1, 4, 1, 4}};
+                                            {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 2, 1, 2, 1, 2, 1, 2, 1, 2, 1, 4, 1, 4, 1, 4}};
 constexpr unsigned char kRowsMode[2][33] = {{1, 1, 1, 1, 1, 1, 1, 1, 1, 13, 1, 13, 13, 9, 5, 5, 13, 1, 13, 5, 1, 5, 5, 5, 5, 5, 5, 5, 5, 5, 13, 13, 13},
-                                              {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 5, 1, 5, 1, 13, 1, 13, 1, 9, 1, 1, 1, 9, 1, 9, 1, 9, 1, 9, 1, 13, 1, 13}};
+                                              {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 5, 1, 5, 1, 5, 1, 5, 1, 9, 1, 9, 1, 9, 1, 9, 1, 9, 1, 13, 1, 13, 1, 13}};
 inline int rows_wg(int n, int b) { return kRowsWG[b == 8][n / 4]; }
 inline int default_mode(int n, int b) { return kRowsMode[b == 8][n / 4]; }
 
