@@ -32,6 +32,13 @@
 #ifndef LAGEN_ROWS_MAXW
 #define LAGEN_ROWS_MAXW 16
 #endif
+// Loads / stores walk warp-per-row when a row's 16-byte pairs fill whole
+// warps, and from this many pairs per row on (the partial second pass idles
+// fewer lanes than the flattened loop's per-element division costs: 4-5 %
+// faster at n = 108..124, 1-9 % slower at n = 68..104; profiles/r01_rowloop_ab.txt)
+#ifndef LAGEN_ROWS_ROWLOOP_H
+#define LAGEN_ROWS_ROWLOOP_H 54
+#endif
 #ifndef LAGEN_ROWS_DBMIN
 #define LAGEN_ROWS_DBMIN 1000  // double-buffer when >= this many slots fit twice (off)
 #endif
@@ -107,7 +114,7 @@ __device__ __forceinline__ void load_rows(double* xs, const double* __restrict__
   // (when a row's pair count is not a multiple of 32 above 32, the flattened
   // loop keeps every lane busy instead)
   constexpr int H = N / 2;
-  if constexpr (H <= 32 || H % 32 == 0) {
+  if constexpr (H <= 32 || H % 32 == 0 || H >= LAGEN_ROWS_ROWLOOP_H) {
     constexpr int NWG = G / 32;
     const int w = rank >> 5, lane = rank & 31;
     for (int r = w; r < N; r += NWG) {
@@ -390,7 +397,7 @@ __device__ __forceinline__ void store_rows(double* __restrict__ dst, const doubl
   // warps over the block row's rows, lanes over 16-byte pairs (coalesced)
   const int nb = r0 + B <= NR ? B : NR - r0;  // real rows of this block row
   constexpr int H = NR / 2;
-  if constexpr (H <= 32 || H % 32 == 0) {
+  if constexpr (H <= 32 || H % 32 == 0 || H >= LAGEN_ROWS_ROWLOOP_H) {
     const int w = rank >> 5, nw = nthr >> 5, lane = rank & 31;
     for (int i = w; i < nb; i += nw) {
       const int r = r0 + i, c0 = 4 * (r >> 2);
@@ -429,6 +436,20 @@ constexpr unsigned char kRowsMode[2][33] = {{1, 1, 1, 1, 1, 1, 1, 1, 1, 13, 1, 1
                                               {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 5, 1, 5, 1, 5, 1, 5, 1, 9, 1, 9, 1, 9, 1, 9, 1, 9, 1, 13, 1, 13, 1, 13}};
 inline int rows_wg(int n, int b) { return kRowsWG[b == 8][n / 4]; }
 inline int default_mode(int n, int b) { return kRowsMode[b == 8][n / 4]; }
+// padded instances (n = 4 mod 8 on the b = 8 kernel of n + 4) where their own
+// sweep (profiles/r01_rowspad_tune.txt) picked a different setting than the
+// unpadded size: {n, WG, mode}
+constexpr int kRowsPadPick[3][3] = {{60, 2, 9}, {76, 2, 13}, {92, 4, 13}};
+inline int pad_wg(int nr) {
+  for (const auto& e : kRowsPadPick)
+    if (e[0] == nr) return e[1];
+  return rows_wg(nr + 4, 8);
+}
+inline int pad_mode(int nr) {
+  for (const auto& e : kRowsPadPick)
+    if (e[0] == nr) return e[2];
+  return default_mode(nr + 4, 8);
+}
 
 template <int N, int B, int WG_, int NR = N>
 __global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)

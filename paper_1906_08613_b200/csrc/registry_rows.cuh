@@ -72,11 +72,11 @@ cudaError_t launch_rows_pad(const LaunchArgs& a, cudaStream_t s) {
   static_assert(N > NR && N % 8 == 0 && NR % 4 == 0, "padding to a multiple of 8");
   static const int mode = [] {
     const char* e = std::getenv("LAGEN_ROWS_MODE");
-    return e ? std::atoi(e) : cr::default_mode(N, 8);
+    return e ? std::atoi(e) : cr::pad_mode(NR);
   }();
   static const int wg = [] {
     const char* e = std::getenv("LAGEN_ROWS_WG");
-    return e ? std::atoi(e) : cr::rows_wg(N, 8);
+    return e ? std::atoi(e) : cr::pad_wg(NR);
   }();
   if (wg == 1) return launch_rows_wg<N, 8, 1, NR>(a, s, mode);
   if (wg == 2) return launch_rows_wg<N, 8, 2, NR>(a, s, mode);
