@@ -35,8 +35,15 @@ struct ColPolicy {
   static constexpr int W = N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : 32;  // lanes per problem
   static constexpr int CPL = N <= 32 ? 1 : 2;                            // columns per lane
   static constexpr int GPW = 32 / W;                                     // problems per warp
-  static constexpr int WARPS = N <= 32 ? 8 : 4;                          // warps per CTA
-  static constexpr int MINB = N <= 32 ? 2 : 1;  // >= 16 warps/SM for n <= 32 (<= 128 regs)
+#ifndef LAGEN_COL_WIDE
+#define LAGEN_COL_WIDE 1
+#endif
+  // n = 28 / 32 as 3 CTAs of 4 warps (12 warps/SM, <= 168 registers): at the
+  // 128-register cap of 16 warps/SM they spilled ~108 bytes per thread;
+  // measured 3-4 % faster (v1) / 11-12 % (v2), profiles/r01_col_wide_ab.txt
+  static constexpr bool WIDE = LAGEN_COL_WIDE && (N == 28 || N == 32);
+  static constexpr int WARPS = WIDE ? 4 : N <= 32 ? 8 : 4;                // warps per CTA
+  static constexpr int MINB = WIDE ? 3 : N <= 32 ? 2 : 1;  // >= 16 warps/SM for n <= 32 (<= 128 regs)
   static constexpr int PUB_LD = 18;  // publish buffer: <= 16 rows per column; even -> LDS.128 pairs
   static constexpr int PUB = PUB_LD * (N < 32 ? N : 32);  // <= 32 columns per publish
   static constexpr int SMEM = WARPS * GPW * PUB * 8;
