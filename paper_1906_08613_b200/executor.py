@@ -88,7 +88,7 @@ def _check_inputs(eq_name, inputs, n=None):
     return shape[0], shape[1]
 
 
-def solve(eq, inputs, variant=None, b=None, out=None, info=None, stream=None, check=True, engine="auto"):
+def solve(eq, inputs, variant=None, b=None, out=None, info=None, stream=None, check=True, engine=None):
     """Solve a batch: inputs in _signature order (chol: A; lyap: L, S;
     sylv: L, U, C), each [batch, n, n] float64 CUDA contiguous.
 
@@ -98,13 +98,18 @@ def solve(eq, inputs, variant=None, b=None, out=None, info=None, stream=None, ch
     that forces a device sync."""
     eq_name = _eq_name(eq)
     batch, n = _check_inputs(eq_name, inputs)
-    stmts, _ = resolve_variant(eq_name, variant)
-    if stmts is None:
+    stmts, idx = resolve_variant(eq_name, variant)
+    if stmts is None:  # the dispatch table's measured (variant, b, engine), like Plan / solve_host
         pick = dispatch.select(eq_name, n)
         stmts = builtin_variants(eq_name)[pick["variant"]].statements
         b = b or pick["b"]
-    if b is None:
-        b = dispatch.select(eq_name, n)["b"]
+        engine = engine or pick.get("engine")
+    elif b is None:
+        pick = dispatch.select(eq_name, n)
+        b = pick["b"]
+        if idx is not None and pick["variant"] == idx:
+            engine = engine or pick.get("engine")
+    engine = engine or "auto"
     validate(eq_name, stmts)
     dev = inputs[0].device
     if out is None:
