@@ -43,7 +43,12 @@ struct ColPolicy {
   // measured 3-4 % faster (v1) / 11-12 % (v2), profiles/r01_col_wide_ab.txt
   static constexpr bool WIDE = LAGEN_COL_WIDE && (N == 28 || N == 32);
   static constexpr int WARPS = WIDE ? 4 : N <= 32 ? 8 : 4;                // warps per CTA
-  static constexpr int MINB = WIDE ? 3 : N <= 32 ? 2 : 1;  // >= 16 warps/SM for n <= 32 (<= 128 regs)
+// n <= 12 fits 3 CTAs of 8 warps (24 warps/SM, <= 85 registers) spill-free:
+// 5-10 % faster at n = 8, 12 (profiles/r01_col_wide_ab.txt)
+#ifndef LAGEN_COL_SMALL3
+#define LAGEN_COL_SMALL3 1
+#endif
+  static constexpr int MINB = WIDE ? 3 : (LAGEN_COL_SMALL3 && N <= 12) ? 3 : N <= 32 ? 2 : 1;  // >= 16 warps/SM for n <= 32 (<= 128 regs)
   static constexpr int PUB_LD = 18;  // publish buffer: <= 16 rows per column; even -> LDS.128 pairs
   static constexpr int PUB = PUB_LD * (N < 32 ? N : 32);  // <= 32 columns per publish
   static constexpr int SMEM = WARPS * GPW * PUB * 8;
