@@ -57,6 +57,10 @@ using eng::lane_id;
 // Residency: WG warps own a problem (a template parameter; the launcher picks
 // it per size, rows_wg()), as many problems per CTA as shared memory allows,
 // double-buffered (next problem prefetched) when >= 6 still fit.
+#ifndef LAGEN_ROWS_SPREAD
+#define LAGEN_ROWS_SPREAD 1
+#endif
+
 template <int N, int WG_>
 struct RPolicy {
   static constexpr int SLOT = N * N / 2 + 2 * N;
@@ -477,7 +481,12 @@ __global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)
   auto slot_at = [&](int d) { return smem + ((size_t)gr.id * P::DB + (d % P::DB)) * P::SLOT; };
   constexpr long long NN = (long long)NR * NR;
   const long long stride = (long long)gridDim.x * P::P;
-  long long prob = (long long)blockIdx.x * P::P + gr.id;
+  // slot-major problem order: round t runs problems [t * stride, (t + 1) * stride)
+  // with slot g of every CTA before slot g + 1 of any, so a partial last round
+  // puts 1-2 problems on every SM (each faster with less contention for the
+  // SM's FP64 / DMMA pipes) instead of full slots on a few SMs
+  long long prob = LAGEN_ROWS_SPREAD ? (long long)gr.id * gridDim.x + blockIdx.x
+                                     : (long long)blockIdx.x * P::P + gr.id;
   if (prob < batch) {
     load_rows<N, G, NR>(slot_at(0), A + prob * NN, gr.rank);
     cp_async_commit();

@@ -191,7 +191,13 @@ __global__ void __launch_bounds__(WPol<EQ, N, NW, PP>::THREADS, 1)
   auto tij = [&](int s) -> int { return (int)((tab[s >> 2] >> (8 * (s & 3))) & 0xff); };
 
   const long long stride = (long long)gridDim.x * PP;
-  for (long long prob = (long long)blockIdx.x * PP + grp; prob < batch; prob += stride) {
+  // slot-major problem order (as in chol_rows.cuh): a partial last round is
+  // spread over every SM instead of filling the slots of a few
+#ifndef LAGEN_WAVE_SPREAD
+#define LAGEN_WAVE_SPREAD 1
+#endif
+  const long long first = LAGEN_WAVE_SPREAD ? (long long)grp * gridDim.x + blockIdx.x : (long long)blockIdx.x * PP + grp;
+  for (long long prob = first; prob < batch; prob += stride) {
     const double* Lp = Lg + prob * NN;
     const double* Up = Ug + prob * NN;
     const double* Cp = Cg + prob * NN;
