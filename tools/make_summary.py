@@ -39,9 +39,9 @@ def main():
            "`" + tag + "_traffic.json`, `" + tag + "_wave_traffic.txt`, `" + tag + "_rows_db.txt`, "
            "`" + tag + "_e2e_bands.txt`; A/B records of this round's tuning: `" + tag + "_chol_lookahead.md`, "
            "`" + tag + "_wave_geometry.md`, `" + tag + "_rows_tune.txt`, `" + tag + "_rowspad_tune.txt`, "
-           "`" + tag + "_rowloop_ab.txt`, `" + tag + "_col_wide_ab.txt`; other BASELINE configs: "
+           "`" + tag + "_rowloop_ab.txt`, `" + tag + "_col_wide_ab.txt`, `" + tag + "_spread_ab.txt`; other BASELINE configs: "
            "`" + tag + "_bench_c1.json` (configs[0]), `" + tag + "_bench_c5.jsonl` (config 5 on one GPU), "
-           "`" + tag + "_bench_reference_arm.json` (`bench.py --impl reference`).", "",
+           "`" + tag + "_bench_reference_arm.json` (`bench.py --impl reference`); GPU parity run of the same tree: `" + tag + "_pytest_gpu_rerun.log` (`tools/gpu_round_end.sh`).", "",
            "## Peaks used", "",
            f"- HBM: {b['peaks']['hbm_gbs']} GB/s ({b['peaks']['source']['hbm_gbs']}).",
            f"- FP64: {b['peaks']['fp64_tflops']} TFLOP/s ({b['peaks']['source']['fp64_tflops']}).", ""]
