@@ -375,6 +375,8 @@ def cpu_baseline(eq, cases, budget_s=12.0, inputs_from=None, seed_first=0):
                    "throughput extrapolated to the full batch; kernel = fastest verified emitted variant "
                    "(lagen emit_function, nu=4) compiled gcc -O3 -march=native -std=c99, OpenMP over problems")
         if use_ref else "oracle C port, OpenMP over problems",
+        "sample_short": (f"first s problems of each size (~{per_size_budget:.2f} s per size), "
+                         "extrapolated to the full batch"),
         "cpu_model": _cpu_model(), "per_n": detail,
     }
 
@@ -391,13 +393,19 @@ def _cpu_model():
 
 # ----------------------------------------------------------------------------
 def summarize(eq, res, steps, peaks, world):
+    """(value, ms_per_step, roofline, per_n) for one sweep.
+
+    roofline: aggregate over the step's launches — the algorithmic bytes (or
+    flops) of every launch (SURVEY §8d per-problem figure x batch) over the
+    sum of their event-timed durations, against the measured peak of the
+    binding roof; "dominant" is the launch with the largest share of the
+    step, with its own achieved / frac and its ncu DRAM traffic."""
     ms = statistics.mean(res["times_ms"])
     ms = max_over_ranks(ms, world)
     flops = sum_over_ranks(res["flops_nominal"], world)
     value = flops / (ms * 1e-3) / 1e9
-    # roofline of the sweep's kernels: algorithmic bytes (or flops) per launch
-    # over the measured launch time, aggregated over the step's launches
-    t_kernels = sum(r["ms"] for r in res["per_n"]) * 1e-3
+    per_n = res["per_n"]
+    t_kernels = sum(r["ms"] for r in per_n) * 1e-3
     achieved_gbs = res["bytes"] / t_kernels / 1e9
     achieved_tf = res["flops_alg"] / t_kernels / 1e12
     hbm_time = res["bytes"] / (peaks["hbm_gbs"] * 1e9)
@@ -408,19 +416,57 @@ def summarize(eq, res, steps, peaks, world):
     else:
         roof = {"bound": "fp64", "achieved": round(achieved_tf, 3), "peak": peaks["fp64_tflops"],
                 "unit": "TFLOP/s", "frac": round(achieved_tf / peaks["fp64_tflops"], 4)}
-    t_roof_nom = sum(r["batch"] * 0 + r["ms"] * r["roofline_frac_nominal"] for r in res["per_n"]) * 1e-3
-    roof["frac_of_nominal_roofline"] = round(t_roof_nom / t_kernels, 4)
-    # DRAM bytes per launch of the profiled kernel (ncu --set full), against
-    # its algorithmic bytes: profiles/r01_traffic.json, written from the
-    # committed ncu captures (the box has no ncu in the timed run)
+    # per-n roofline (time at the binding measured roof / measured time),
+    # aggregated as roof time over kernel time
+    t_roof = sum(r["ms"] * r["roofline_frac_measured"] for r in per_n) * 1e-3
+    roof["frac_roofline_time"] = round(t_roof / t_kernels, 4)
+    roof["frac_min_n_ge_32"] = min((r["roofline_frac_measured"] for r in per_n if r["n"] >= 32), default=None)
+    dom = max(per_n, key=lambda r: r["ms"])
+    roof["dominant"] = {"n": dom["n"], "engine": dom["engine"], "share": round(dom["ms"] * 1e-3 / t_kernels, 3),
+                        "gbs": dom["gbs"], "frac": dom["roofline_frac_measured"]}
+    roof["scope"] = "all launches of one step (sum of algorithmic bytes / sum of launch times)"
     roof["traffic"] = None
-    tf = REPO / "profiles" / "r01_traffic.json"
-    if tf.exists():
-        t = json.loads(tf.read_text()).get(eq)
-        if t:
-            roof["traffic"] = t["dram_bytes_per_launch"]
-            roof["traffic_kernel"] = {k: t[k] for k in ("kernel", "algorithmic_bytes_per_launch", "ratio", "source")}
-    return value, ms, roof
+    for tf in (REPO / "profiles" / "r02_traffic.json", REPO / "profiles" / "r01_traffic.json"):
+        if tf.exists():
+            t = json.loads(tf.read_text()).get(eq)
+            if t:
+                roof["traffic"] = t["dram_bytes_per_launch"]
+                roof["traffic_ratio"] = t["ratio"]
+                roof["traffic_of"] = f"n={t['n']} ({tf.name})"
+                break
+    return value, ms, roof, per_n
+
+
+def cpu_compact(c):
+    return {k: c[k] for k in ("value", "unit", "cores", "kind")} | {"sample": c["sample_short"]}
+
+
+def run_one(wl, args, world, rank, peaks, warmup, clocks=None, want_e2e=True, want_cpu=True):
+    eq, cases, scaling, desc = workload(wl, world, rank)
+    res = run_sweep(eq, cases, rank, args.steps, warmup, peaks, flush_l2=(wl == "c1"), clocks=clocks)
+    value, ms, roof, per_n = summarize(eq, res, args.steps, peaks, world)
+    out = {"eq": eq, "value": value, "ms": ms, "roofline": roof, "per_n": per_n, "desc": desc,
+           "scaling": scaling, "sizes": [c[0] for c in cases], "launches": res["launches_per_step"]}
+    if want_e2e and not args.no_e2e:
+        e2e_steps = max(1, min(2, args.steps))
+        dt, h2d, d2h = run_e2e(eq, res["plans"], e2e_steps, world)
+        out["e2e"] = {"value": round(sum_over_ranks(res["flops_nominal"], world) / dt / 1e9, 2),
+                      "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    if want_cpu and rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu"] = cpu_baseline(eq, cases, budget_s=args.cpu_budget, inputs_from=[p.inputs for p in res["plans"]])
+    del res
+    torch.cuda.empty_cache()
+    return out
+
+
+def spawn_ranks(gpus):
+    """--gpus N > 1 without a launcher: re-exec this script under
+    torch.distributed.run with N processes (one per GPU)."""
+    port = os.environ.get("MASTER_PORT", "29533")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", port, str(Path(__file__).resolve()), *sys.argv[1:]]
+    import subprocess
+    return subprocess.call(cmd)
 
 
 def main():
@@ -434,84 +480,134 @@ def main():
     ap.add_argument("--no-extra", action="store_true", help="skip the lyap/sylv sweeps")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--json-out", default=None)
+    ap.add_argument("--cpu-budget", type=float, default=8.0)
+    ap.add_argument("--json-out", default=None, help="full per-n detail (the printed line stays compact)")
+    ap.add_argument("--stub", action="store_true",
+                    help="CPU-only dry run of the distributed plumbing (gloo, no kernels); tests only")
     args = ap.parse_args()
     if args.sizes:
         global SIZES
         SIZES = [int(x) for x in args.sizes.split(",")]
     warmup = max(3, args.warmup)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return reference_arm(args, warmup)
+    if args.stub:
+        return stub_arm(args, warmup)
 
     world, rank, local = dist_setup(args.gpus)
+    if args.gpus > 1 and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     peaks = measured_peaks()
-    eq, cases, scaling, desc = workload(args.workload, world, rank)
     clocks = ClockSampler(local)
     barrier(world)
-    res = run_sweep(eq, cases, rank, args.steps, warmup, peaks, flush_l2=(args.workload == "c1"),
-                    clocks=clocks)
-    value, ms, roof = summarize(eq, res, args.steps, peaks, world)
+    head = run_one(args.workload, args, world, rank, peaks, warmup, clocks=clocks)
+    extra = {}
+    if args.workload == "chol-sweep" and not args.no_extra:
+        for wl in ("lyap-sweep", "sylv-sweep"):
+            extra[wl] = run_one(wl, args, world, rank, peaks, warmup)
     line = {
-        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-        "scaling": scaling, "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: seeded counter-based generator, BASELINE.json distributions (no dataset)",
-        "config": {"workload": args.workload, "description": desc, "sizes": [c[0] for c in cases],
-                   "batch_per_gpu": {str(c[0]): c[1] for c in cases},
+        "metric": METRIC, "value": round(head["value"], 2), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": warmup, "ms_per_step": round(head["ms"], 4), "higher_is_better": True,
+        "scaling": head["scaling"], "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, BASELINE.json distributions)",
+        "config": {"workload": args.workload, "description": head["desc"],
+                   "sizes": _sizes_text(head["sizes"]),
                    "l2": "flush 256 MiB between steps" if args.workload == "c1" else
                    "inputs > L2 (>= 256 MiB per operand per size)",
-                   "variant_selection": "dispatch_table.json (GPU autotune of every variant x b) "
-                                        "else static fallback",
-                   "timing": "sweep captured in one CUDA graph; CUDA events on the launching stream"},
-        "roofline": roof,
-        "gpu_launches": res["launches_per_step"] * args.steps,
+                   "parallelism": f"shard by problem index x{world}, no collective"},
+        "roofline": head["roofline"],
+        "gpu_launches": head["launches"] * args.steps,
         "clocks": clocks.summary(),
-        "peaks": peaks,
-        "per_n": res["per_n"],
     }
-    if not args.no_e2e:
-        e2e_steps = max(1, min(2, args.steps))
-        dt, h2d, d2h = run_e2e(eq, res["plans"], e2e_steps, world)
-        line["e2e"] = {"value": round(sum_over_ranks(res["flops_nominal"], world) / dt / 1e9, 2),
-                       "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                       "steps": e2e_steps,
-                       "path": "executor.solve_host -> lagen_b200_execute_host_engine (pinned host buffers, "
-                               "chunked H2D/solve/D2H over four persistent streams)"}
-    if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(eq, cases, budget_s=args.cpu_budget,
-                                            inputs_from=[p.inputs for p in res["plans"]])
-    # free before the secondary sweeps
-    del res
-    torch.cuda.empty_cache()
-    if args.workload == "chol-sweep" and not args.no_extra:
-        extra = {}
-        for wl in ("lyap-sweep", "sylv-sweep"):
-            eq2, cases2, _, desc2 = workload(wl, world, rank)
-            r2 = run_sweep(eq2, cases2, rank, args.steps, warmup, peaks)
-            v2, ms2, roof2 = summarize(eq2, r2, args.steps, peaks, world)
-            extra[eq2] = {"value": round(v2, 2), "unit": "GFLOP/s", "ms_per_step": round(ms2, 4),
-                          "roofline": roof2, "per_n": r2["per_n"], "description": desc2}
-            if rank == 0 and world == 1 and not args.no_cpu:
-                extra[eq2]["cpu_baseline"] = cpu_baseline(eq2, cases2, budget_s=args.cpu_budget,
-                                                          inputs_from=[p.inputs for p in r2["plans"]])
-            del r2
-            torch.cuda.empty_cache()
-        line["extra"] = extra
+    if "e2e" in head:
+        line["e2e"] = head["e2e"]
+    if "cpu" in head:
+        line["cpu_baseline"] = cpu_compact(head["cpu"])
+    if extra:
+        line["extra"] = {}
+        for wl, r in extra.items():
+            e = {"value": round(r["value"], 2), "ms_per_step": round(r["ms"], 3),
+                 "roofline_frac": r["roofline"]["frac"], "roofline_bound": r["roofline"]["bound"],
+                 "frac_roofline_time": r["roofline"]["frac_roofline_time"],
+                 "frac_min_n_ge_32": r["roofline"]["frac_min_n_ge_32"]}
+            if "e2e" in r:
+                e["e2e"] = r["e2e"]["value"]
+            if "cpu" in r:
+                e["cpu_baseline"] = r["cpu"]["value"]
+            line["extra"][r["eq"]] = e
     if rank == 0:
-        text = json.dumps(line)
-        print(text, flush=True)
+        print(json.dumps(line, separators=(",", ":")), flush=True)
         if args.json_out:
-            Path(args.json_out).write_text(json.dumps(line, indent=1) + "\n")
+            detail = dict(line)
+            detail["peaks"] = peaks
+            detail["per_n"] = head["per_n"]
+            if "cpu" in head:
+                detail["cpu_baseline_detail"] = head["cpu"]
+            detail["extra_detail"] = {r["eq"]: {"per_n": r["per_n"], "roofline": r["roofline"],
+                                                "cpu": r.get("cpu"), "e2e": r.get("e2e")}
+                                      for r in extra.values()}
+            Path(args.json_out).write_text(json.dumps(detail, indent=1) + "\n")
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
+def _sizes_text(sizes):
+    if len(sizes) > 3 and all(b - a == sizes[1] - sizes[0] for a, b in zip(sizes, sizes[1:])):
+        return f"{sizes[0]}..{sizes[-1]} step {sizes[1] - sizes[0]}"
+    return ",".join(map(str, sizes))
+
+
+def stub_arm(args, warmup):
+    """The distributed plumbing of the GPU arm (rank setup, barrier, per-rank
+    shard, max-over-ranks time, whole-job sum, rank-0 line) with a CPU stub
+    in place of the kernels, under gloo — exercised by tests/test_bench_dist.py."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        torch.distributed.init_process_group("gloo")
+    eq, cases, scaling, desc = workload(args.workload, world, rank)
+    flops = 0.0
+    for n, batch, seed, first in cases:
+        flops += batch * _nominal(eq, n)
+    dts = []
+    for i in range(warmup + args.steps):
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        time.sleep(0.001 * (rank + 1))  # rank-dependent "device time"
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            dts.append(dt)
+    ms = statistics.mean(dts) * 1e3
+    t = torch.tensor([ms, flops], dtype=torch.float64)
+    if world > 1:
+        mx = t[:1].clone()
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        sm = t[1:].clone()
+        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+        ms, flops = float(mx.item()), float(sm.item())
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+                          "n_gpus": world, "steps": args.steps, "warmup": warmup, "ms_per_step": ms,
+                          "scaling": scaling, "stub": True,
+                          "config": {"workload": args.workload, "first_index": [c[3] for c in cases][:1]}}),
+              flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def _nominal(eq, n):
+    return n ** 3 / 3 if eq == "cholesky" else 2.0 * n ** 3
+
+
 def reference_arm(args, warmup):
     """The reference's own CPU implementation of the path (oracle/_ref: the
-    emitted kernels compiled here with the reference's flags) on the host
-    cores, same workload/metric; rank 0 only."""
+    emitted kernels compiled with the reference's flags) on the host cores,
+    same workload / metric; rank 0 only (other ranks exit 0 without work)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
@@ -533,11 +629,11 @@ def reference_arm(args, warmup):
     line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": warmup, "ms_per_step": round(dt / args.steps * 1e3, 2), "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: seeded counter-based generator (CPU twin), BASELINE.json distributions",
-            "config": {"workload": args.workload, "description": desc, "sizes": [c[0] for c in cases]},
-            "impl": "reference", "cpu_baseline": base,
+            "data": "synthetic (seeded generator CPU twin, BASELINE.json distributions)",
+            "config": {"workload": args.workload, "description": desc, "sizes": _sizes_text([c[0] for c in cases])},
+            "impl": "reference", "cpu_baseline": cpu_compact(base),
             "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line, separators=(",", ":")), flush=True)
     return 0
 
 

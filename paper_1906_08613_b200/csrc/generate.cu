@@ -90,15 +90,21 @@ __global__ void gen_spd(int n, uint64_t key, long long first, long long batch, d
   }
 }
 
-thread_local std::string g_gen_error;
-
 }  // namespace
+
+namespace lagen {
+int set_error(int code, const std::string& msg);  // lagen_b200.cu
+}
+using lagen::set_error;
 
 extern "C" int lagen_b200_generate(int eq, int n, unsigned long long seed, long long first, long long batch,
                                    double* const* outputs, void* stream) {
-  if (eq < 0 || eq > 2 || n < 1 || n > 128 || batch < 0 || first < 0 || !outputs) return LAGEN_EINVAL;
+  if (eq < 0 || eq > 2) return set_error(LAGEN_EINVAL, "generate: unknown equation");
+  if (n < 1 || n > 128) return set_error(LAGEN_EINVAL, "generate: n must be in 1..128");
+  if (batch < 0 || first < 0) return set_error(LAGEN_EINVAL, "generate: negative batch or first index");
+  if (!outputs) return set_error(LAGEN_EINVAL, "generate: null output array");
   for (int i = 0; i <= eq; ++i)
-    if (!outputs[i]) return LAGEN_EINVAL;
+    if (!outputs[i]) return set_error(LAGEN_EINVAL, "generate: null output buffer");
   if (batch == 0) return LAGEN_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t key = gen_key(seed, eq, n);
@@ -106,7 +112,7 @@ extern "C" int lagen_b200_generate(int eq, int n, unsigned long long seed, long 
     const int smem = n * n * 8;
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(gen_spd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return LAGEN_ECUDA;
+      if (e != cudaSuccess) return set_error(LAGEN_ECUDA, std::string("generate: ") + cudaGetErrorString(e));
     }
     long long grid = batch < 148 * 64 ? batch : 148 * 64;
     gen_spd<<<(unsigned)grid, 256, smem, s>>>(n, key, first, batch, outputs[0]);
@@ -117,5 +123,7 @@ extern "C" int lagen_b200_generate(int eq, int n, unsigned long long seed, long 
     gen_elementwise<<<(unsigned)grid, 256, 0, s>>>(eq, n, key, first, batch, outputs[0], outputs[1],
                                                   eq == LAGEN_SYLVESTER ? outputs[2] : nullptr);
   }
-  return cudaGetLastError() == cudaSuccess ? LAGEN_OK : LAGEN_ECUDA;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(LAGEN_ECUDA, std::string("generate launch: ") + cudaGetErrorString(e));
+  return LAGEN_OK;
 }

@@ -25,13 +25,21 @@
 using namespace lagen;
 
 namespace {
-
 thread_local std::string g_last_error;
+}  // namespace
 
-int fail(int code, const std::string& msg) {
+namespace lagen {
+// shared with generate.cu: every failing entry point sets the message that
+// lagen_b200_last_error() returns
+int set_error(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+}  // namespace lagen
+
+namespace {
+
+int fail(int code, const std::string& msg) { return lagen::set_error(code, msg); }
 
 int cuda_fail(cudaError_t e, const char* where) {
   return fail(LAGEN_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -220,15 +228,32 @@ int check_common(int eq, int n, int b, long long batch) {
   return LAGEN_OK;
 }
 
-// problem p, element (r, c) of the n' x n' padded operand
+// problem p, element (r, c) of the n' x n' padded operand.  Padded diagonal:
+// 0 for a right-hand side, 1 for the Cholesky A, and for a Lyapunov /
+// Sylvester coefficient d = 1 + max |diagonal| over the problem's L (and U),
+// so every padded pivot (d + u_jj, l_ii + d, 2d) is nonzero (a fixed 1 gives
+// 0 / 0 when a real diagonal entry is -1).
 __global__ void pad_kernel(const double* __restrict__ src, double* __restrict__ dst, long long batch, int n, int np,
-                           double diag) {
+                           int mode, const double* __restrict__ co0, const double* __restrict__ co1) {
   const long long total = batch * np * np;
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < total;
        u += (long long)gridDim.x * blockDim.x) {
     const long long p = u / (np * np);
     const int e = (int)(u - p * np * np), r = e / np, c = e - r * np;
-    dst[u] = (r < n && c < n) ? src[(p * n + r) * n + c] : (r == c ? diag : 0.0);
+    double v = 0.0;
+    if (r < n && c < n) {
+      v = src[(p * n + r) * n + c];
+    } else if (r == c && mode == 1) {
+      v = 1.0;
+    } else if (r == c && mode == 2) {
+      double m = 0.0;
+      for (int i = 0; i < n; ++i) {
+        m = fmax(m, fabs(co0[(p * n + i) * n + i]));
+        if (co1) m = fmax(m, fabs(co1[(p * n + i) * n + i]));
+      }
+      v = 1.0 + m;
+    }
+    dst[u] = v;
   }
 }
 
@@ -353,10 +378,13 @@ int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int 
     cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(double) * per * (nin + 1), s);
     if (err != cudaSuccess) return cuda_fail(err, "padded buffers");
     const double* pin[3] = {nullptr, nullptr, nullptr};
-    // identity on the diagonal of L, U and A; zeros in S and C
+    // identity on the diagonal of A, a per-problem nonzero-pivot value on the
+    // diagonal of L and U, zeros in S and C
     for (int i = 0; i < nin; ++i) {
       const bool rhs = (eq == LAGEN_LYAPUNOV && i == 1) || (eq == LAGEN_SYLVESTER && i == 2);
-      pad_kernel<<<grid_for((long long)per), 256, 0, s>>>(inputs[i], buf + per * i, batch, n, np, rhs ? 0.0 : 1.0);
+      const int mode = rhs ? 0 : (eq == LAGEN_CHOLESKY ? 1 : 2);
+      pad_kernel<<<grid_for((long long)per), 256, 0, s>>>(inputs[i], buf + per * i, batch, n, np, mode, inputs[0],
+                                                          eq == LAGEN_SYLVESTER ? inputs[1] : nullptr);
       pin[i] = buf + per * i;
     }
     double* Xp = buf + per * nin;

@@ -57,6 +57,29 @@ def resolve_variant(eq_name, variant):
     return list(variant), None
 
 
+def _resolve(eq_name, n, variant, b, engine):
+    """(stmts, variant_index, b, engine) for a solve: the dispatch table's
+    measured (variant, b, engine) fills what the caller left open.  The
+    table's engine is used only when it runs the requested (variant, b)
+    (it was chosen for the table's b); otherwise "auto"."""
+    stmts, idx = resolve_variant(eq_name, variant)
+    pick = dispatch.select(eq_name, n)
+    if stmts is None:
+        idx = pick["variant"]
+        stmts = builtin_variants(eq_name)[idx].statements
+    if b is None:
+        b = pick["b"]
+    if engine is None:
+        engine = "auto"
+        table_engine = pick.get("engine") or "auto"
+        if idx is not None and idx == pick["variant"] and table_engine != "auto":
+            if b == pick["b"] or _lib.engine_supported(EQ_CODES[eq_name], n, b, idx, table_engine):
+                engine = table_engine
+    if engine not in _lib.ENGINES:
+        raise errors.UsageError(f"unknown engine {engine!r}; one of {sorted(_lib.ENGINES)}")
+    return stmts, idx, b, engine
+
+
 def _stream_ptr(stream):
     if stream is None:
         stream = torch.cuda.current_stream()
@@ -98,18 +121,7 @@ def solve(eq, inputs, variant=None, b=None, out=None, info=None, stream=None, ch
     that forces a device sync."""
     eq_name = _eq_name(eq)
     batch, n = _check_inputs(eq_name, inputs)
-    stmts, idx = resolve_variant(eq_name, variant)
-    if stmts is None:  # the dispatch table's measured (variant, b, engine), like Plan / solve_host
-        pick = dispatch.select(eq_name, n)
-        stmts = builtin_variants(eq_name)[pick["variant"]].statements
-        b = b or pick["b"]
-        engine = engine or pick.get("engine")
-    elif b is None:
-        pick = dispatch.select(eq_name, n)
-        b = pick["b"]
-        if idx is not None and pick["variant"] == idx:
-            engine = engine or pick.get("engine")
-    engine = engine or "auto"
+    stmts, idx, b, engine = _resolve(eq_name, n, variant, b, engine)
     validate(eq_name, stmts)
     dev = inputs[0].device
     if out is None:
@@ -123,7 +135,7 @@ def solve(eq, inputs, variant=None, b=None, out=None, info=None, stream=None, ch
                                                 batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
                                                 ctypes.c_void_p(info.data_ptr()), _stream_ptr(stream),
                                                 _lib.ENGINES[engine])
-    _lib.check(rc, f"{eq_name} n={n} b={b}")
+    _lib.check(rc, f"{eq_name} n={n} b={b} engine={engine}")
     if check and batch:
         bad = torch.nonzero(info).flatten()
         if bad.numel():
@@ -143,18 +155,10 @@ class Plan:
     def __init__(self, eq, inputs, variant=None, b=None, out=None, info=None, engine=None):
         self.eq = _eq_name(eq)
         self.batch, self.n = _check_inputs(self.eq, inputs)
-        stmts, idx = resolve_variant(self.eq, variant)
-        if stmts is None:
-            pick = dispatch.select(self.eq, self.n)
-            idx = pick["variant"]
-            stmts = builtin_variants(self.eq)[idx].statements
-            b = b or pick["b"]
-            engine = engine or pick.get("engine")
-        if b is None:
-            b = dispatch.select(self.eq, self.n)["b"]
+        stmts, idx, b, engine = _resolve(self.eq, self.n, variant, b, engine)
         validate(self.eq, stmts)
         self.variant, self.b, self.stmts = idx, b, stmts
-        self.engine = engine or "auto"
+        self.engine = engine
         dev = inputs[0].device
         self.inputs = list(inputs)
         self.out = out if out is not None else torch.empty((self.batch, self.n, self.n),
@@ -214,37 +218,41 @@ def solve_host(eq, inputs, variant=None, b=None, out=None, info=None, engine=Non
     Streams the batch through the GPU with H2D / solve / D2H overlap; runs the
     same kernel as solve() (dispatch-table engine unless given)."""
     eq_name = _eq_name(eq)
+    names = EQ_INPUTS[eq_name]
+    if len(inputs) != len(names):
+        raise errors.UsageError(f"{eq_name} takes inputs {names}, got {len(inputs)} arrays")
     arrs = []
-    for t in inputs:
+    for nm, t in zip(names, inputs):
         if isinstance(t, torch.Tensor):
             if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
-                raise errors.UsageError("host inputs must be contiguous float64 CPU tensors")
+                raise errors.UsageError(f"host input {nm} must be a contiguous float64 CPU tensor")
             arrs.append(t)
         else:
             a = np.ascontiguousarray(t, dtype=np.float64)
             arrs.append(torch.from_numpy(a))
-    batch, n = arrs[0].shape[0], arrs[0].shape[1]
-    stmts, idx = resolve_variant(eq_name, variant)
-    if stmts is None:
-        pick = dispatch.select(eq_name, n)
-        stmts = builtin_variants(eq_name)[pick["variant"]].statements
-        b = b or pick["b"]
-        engine = engine or pick.get("engine")
-    elif b is None:
-        pick = dispatch.select(eq_name, n)
-        b = pick["b"]
-        if idx is not None and pick["variant"] == idx:
-            engine = engine or pick.get("engine")
+    shape = tuple(arrs[0].shape)
+    if len(shape) != 3 or shape[1] != shape[2]:
+        raise errors.UsageError(f"host inputs must be [batch, n, n], got {shape}")
+    if any(tuple(a.shape) != shape for a in arrs):
+        raise errors.UsageError("host inputs disagree in shape")
+    batch, n = shape[0], shape[1]
+    stmts, idx, b, engine = _resolve(eq_name, n, variant, b, engine)
     validate(eq_name, stmts)
     if out is None:
         out = torch.empty((batch, n, n), dtype=torch.float64, pin_memory=arrs[0].is_pinned())
+    elif (not isinstance(out, torch.Tensor) or out.is_cuda or out.dtype != torch.float64
+          or tuple(out.shape) != shape or not out.is_contiguous()):
+        raise errors.UsageError(f"out must be a contiguous float64 CPU tensor of shape {shape}")
     if info is None:
         info = torch.empty(batch, dtype=torch.int32)
+    elif (not isinstance(info, torch.Tensor) or info.is_cuda or info.dtype != torch.int32
+          or info.numel() < batch or not info.is_contiguous()):
+        raise errors.UsageError(f"info must be a contiguous int32 CPU tensor with >= {batch} entries")
     arr = _lib.stmt_array(stmts)
     ptrs = (ctypes.c_void_p * 3)(*([t.data_ptr() for t in arrs] + [0] * (3 - len(arrs))))
     rc = _lib.lib.lagen_b200_execute_host_engine(EQ_CODES[eq_name], ctypes.addressof(arr), len(stmts), n, b,
                                                  batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
-                                                 ctypes.c_void_p(info.data_ptr()), _lib.ENGINES[engine or "auto"])
+                                                 ctypes.c_void_p(info.data_ptr()), _lib.ENGINES[engine])
     _lib.check(rc, f"{eq_name} host n={n} b={b}")
     return out, info
 
