@@ -138,6 +138,14 @@ int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b
  * identity-padded problem (n = 4 mod 8 -> n + 4; 104 -> 112; 120 -> 128;
  * only the real n x n entries move) */
 #define LAGEN_ENGINE_ROWS_PAD 7
+/* Lyapunov v5 / Sylvester v13 order at 8x8-tile granularity: dedicated
+ * solver warps solve anti-diagonal d while updater warps apply diagonal
+ * d-1's DMMA tile updates (pipe.cuh) */
+#define LAGEN_ENGINE_PIPE 8
+/* Lyapunov / Sylvester at b = n, n <= 32 (the SYLV / LYAP leaf on the whole
+ * matrix, kernels.py:100-130): one lane per row, column-by-column forward
+ * substitution with the X U part lane-local (rowsweep.cuh); any variant */
+#define LAGEN_ENGINE_ROWSWEEP 9
 int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
                               long long batch, const double* const* inputs, double* X,
                               int* info, void* stream, int engine);

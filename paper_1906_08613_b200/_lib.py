@@ -64,7 +64,7 @@ EXPORTED = (
     "lagen_b200_execute_engine", "lagen_b200_warp_supported", "lagen_b200_engine_supported",
     "lagen_b200_execute_profile", "lagen_b200_host_bytes",
 )
-ENGINES = {"auto": 0, "generic": 1, "warp": 2, "column": 3, "dataflow": 4, "rows": 5, "wave": 6, "rowspad": 7}
+ENGINES = {"auto": 0, "generic": 1, "warp": 2, "column": 3, "dataflow": 4, "rows": 5, "wave": 6, "rowspad": 7, "pipe": 8, "rowsweep": 9}
 
 
 def host_bytes(eq_code, n, batch):

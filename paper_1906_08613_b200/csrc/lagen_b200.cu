@@ -20,6 +20,8 @@
 #include "registry_rows.cuh"
 #include "registry_warp.cuh"
 #include "registry_wave.cuh"
+#include "registry_pipe.cuh"
+#include "registry_rowsweep.cuh"
 #include "variants_table.h"
 
 using namespace lagen;
@@ -104,6 +106,32 @@ const WaveEntry* find_wave(int eq, int n, int b, int variant) {
   if (!((eq == 1 && variant == 5) || (eq == 2 && variant == 13))) return nullptr;
   for (int p = 0; p < kWaveParts; ++p) {
     const WaveTable& t = kWaveTables[p];
+    for (int i = 0; i < *t.n; ++i)
+      if (t.e[i].eq == eq && t.e[i].n == n) return &t.e[i];
+  }
+  return nullptr;
+}
+
+// pipe engine: Lyapunov v5 / Sylvester v13 order at 8x8-tile granularity
+// (pipe.cuh), any block size the variant runs at
+const PipeEntry* find_pipe(int eq, int n, int b, int variant) {
+  (void)b;
+  if (!((eq == 1 && variant == 5) || (eq == 2 && variant == 13))) return nullptr;
+  for (int p = 0; p < kPipeParts; ++p) {
+    const PipeTable& t = kPipeTables[p];
+    for (int i = 0; i < *t.n; ++i)
+      if (t.e[i].eq == eq && t.e[i].n == n) return &t.e[i];
+  }
+  return nullptr;
+}
+
+// rowsweep engine: Lyapunov / Sylvester n <= 32 as the b = n leaf (the SYLV
+// / LYAP block kernel on the whole matrix, rowsweep.cuh) — every variant
+// reduces to that single statement at b = n
+const RowSweepEntry* find_rowsweep(int eq, int n, int b, int variant) {
+  if (eq < 1 || eq > 2 || variant < 0 || b != n) return nullptr;
+  for (int p = 0; p < kRowSweepParts; ++p) {
+    const RowSweepTable& t = kRowSweepTables[p];
     for (int i = 0; i < *t.n; ++i)
       if (t.e[i].eq == eq && t.e[i].n == n) return &t.e[i];
   }
@@ -217,12 +245,12 @@ int padded_size(int eq, int n, int b, int* bp) {
   return 0;
 }
 
-int check_common(int eq, int n, int b, long long batch) {
+int check_common(int eq, int n, int b, long long batch, bool direct = false) {
   if (eq < 0 || eq > 2) return fail(LAGEN_EINVAL, "unknown equation");
   if (batch < 0) return fail(LAGEN_EINVAL, "negative batch");
   if (n < 1 || b < 1 || n % b) return fail(LAGEN_EUNSUPPORTED, "block size does not divide n");
   int bp = 0;
-  if (!find_entry(eq, n, b) && !padded_size(eq, n, b, &bp))
+  if (!direct && !find_entry(eq, n, b) && !padded_size(eq, n, b, &bp))
     return fail(LAGEN_EUNSUPPORTED, "no sm_100a instance for (n=" + std::to_string(n) + ", b=" +
                                         std::to_string(b) + ")");
   return LAGEN_OK;
@@ -342,6 +370,8 @@ int lagen_b200_engine_supported(int eq, int n, int b, int variant, int engine) {
     case LAGEN_ENGINE_ROWS: return find_rows(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_WAVE: return find_wave(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_ROWS_PAD: return find_rows_pad(eq, n, b, variant) ? 1 : 0;
+    case LAGEN_ENGINE_PIPE: return find_pipe(eq, n, b, variant) ? 1 : 0;
+    case LAGEN_ENGINE_ROWSWEEP: return find_rowsweep(eq, n, b, variant) ? 1 : 0;
   }
   return 0;
 }
@@ -359,16 +389,22 @@ int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n
 int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                const double* const* inputs, double* X, int* info, void* stream, int engine,
                                unsigned long long* d_prof) {
-  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWS_PAD) return fail(LAGEN_EINVAL, "unknown engine");
-  int rc = check_common(eq, n, b, batch);
+  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWSWEEP) return fail(LAGEN_EINVAL, "unknown engine");
+  int rc = validate(eq, stmts, nstmts);
   if (rc) return rc;
-  rc = validate(eq, stmts, nstmts);
+  // engines with their own instance for (n, b) that the generic table lacks
+  // (rowsweep: b = n) run directly, without padding
+  const RowSweepEntry* rs_direct =
+      (engine == LAGEN_ENGINE_ROWSWEEP || engine == LAGEN_ENGINE_AUTO) && eq >= 1 && eq <= 2 && b == n
+          ? find_rowsweep(eq, n, b, match_builtin(eq, stmts, nstmts))
+          : nullptr;
+  rc = check_common(eq, n, b, batch, rs_direct != nullptr);
   if (rc) return rc;
   if (batch == 0) return LAGEN_OK;
   if (!inputs || !X) return fail(LAGEN_EINVAL, "null buffer");
   for (int i = 0; i < eq_ninputs(eq); ++i)
     if (!inputs[i]) return fail(LAGEN_EINVAL, "null input buffer");
-  if (!find_entry(eq, n, b)) {  // identity-padded problem (see padded_size)
+  if (!rs_direct && !find_entry(eq, n, b)) {  // identity-padded problem (see padded_size)
     int bp = 0;
     const int np = padded_size(eq, n, b, &bp);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -406,7 +442,10 @@ int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int 
   a.info = info;
   a.batch = batch;
   a.prof = d_prof;
-  LaunchFn fn = find_entry(eq, n, b)->launch;
+  const KernelEntry* ge = find_entry(eq, n, b);
+  if (!ge && !rs_direct) return fail(LAGEN_EUNSUPPORTED, "no sm_100a instance");
+  if (engine == LAGEN_ENGINE_GENERIC && !ge) return fail(LAGEN_EUNSUPPORTED, "no generic instance for this (n, b)");
+  LaunchFn fn = ge ? ge->launch : rs_direct->launch;
   if (engine != LAGEN_ENGINE_GENERIC) {
     const int v = match_builtin(eq, stmts, nstmts);
     const ColEntry* c = (engine == LAGEN_ENGINE_AUTO || engine == LAGEN_ENGINE_COLUMN) ? find_col(eq, n, b, v) : nullptr;
@@ -426,14 +465,26 @@ int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int 
       return fail(LAGEN_EUNSUPPORTED, "no rows-engine instance for this (variant, n, b)");
     // AUTO: the wave engine for the right-looking Lyapunov / Sylvester
     // variants at n >= 16 (dispatch_table.json measures the rest)
-    const WaveEntry* wv =
-        (engine == LAGEN_ENGINE_WAVE || (engine == LAGEN_ENGINE_AUTO && n >= 16)) ? find_wave(eq, n, b, v) : nullptr;
+    // AUTO: the pipe engine for the right-looking Lyapunov / Sylvester
+    // variants (dispatch_table.json measures the rest)
+    const PipeEntry* pp =
+        (engine == LAGEN_ENGINE_PIPE || engine == LAGEN_ENGINE_AUTO) ? find_pipe(eq, n, b, v) : nullptr;
+    if (engine == LAGEN_ENGINE_PIPE && !pp)
+      return fail(LAGEN_EUNSUPPORTED, "no pipe-engine instance for this (variant, n, b)");
+    const WaveEntry* wv = (engine == LAGEN_ENGINE_WAVE) ? find_wave(eq, n, b, v) : nullptr;
+    // AUTO: the rowsweep engine whenever b = n (n <= 32)
+    const RowSweepEntry* rs =
+        (engine == LAGEN_ENGINE_ROWSWEEP || engine == LAGEN_ENGINE_AUTO) ? find_rowsweep(eq, n, b, v) : nullptr;
+    if (engine == LAGEN_ENGINE_ROWSWEEP && !rs)
+      return fail(LAGEN_EUNSUPPORTED, "no rowsweep-engine instance for this (variant, n, b): it runs b = n, n <= 32");
     if (engine == LAGEN_ENGINE_WAVE && !wv)
       return fail(LAGEN_EUNSUPPORTED, "no wave-engine instance for this (variant, n, b)");
     const RowsEntry* rp = (engine == LAGEN_ENGINE_ROWS_PAD) ? find_rows_pad(eq, n, b, v) : nullptr;
     if (engine == LAGEN_ENGINE_ROWS_PAD && !rp)
       return fail(LAGEN_EUNSUPPORTED, "no padded rows-engine instance for this (variant, n, b)");
     if (rp) fn = rp->launch;
+    else if (rs) fn = rs->launch;
+    else if (pp) fn = pp->launch;
     else if (wv) fn = wv->launch;
     else if (st) fn = st->launch;
     else if (d) fn = d->launch;
@@ -549,10 +600,16 @@ int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, 
 
 int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                    const double* const* h_inputs, double* h_X, int* h_info, int engine) {
-  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWS_PAD) return fail(LAGEN_EINVAL, "unknown engine");
-  int rc = check_common(eq, n, b, batch);
+  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWSWEEP) return fail(LAGEN_EINVAL, "unknown engine");
+  int rc = validate(eq, stmts, nstmts);
   if (rc) return rc;
-  rc = validate(eq, stmts, nstmts);
+  // engines with their own instance for (n, b) that the generic table lacks
+  // (rowsweep: b = n) run directly, without padding
+  const RowSweepEntry* rs_direct =
+      (engine == LAGEN_ENGINE_ROWSWEEP || engine == LAGEN_ENGINE_AUTO) && eq >= 1 && eq <= 2 && b == n
+          ? find_rowsweep(eq, n, b, match_builtin(eq, stmts, nstmts))
+          : nullptr;
+  rc = check_common(eq, n, b, batch, rs_direct != nullptr);
   if (rc) return rc;
   if (batch == 0) return LAGEN_OK;
   if (!h_inputs || !h_X) return fail(LAGEN_EINVAL, "null buffer");

@@ -33,6 +33,7 @@ for n in [int(x) for x in a.sizes.split(",")]:
     for r in a.runs.split(","):
         v, b, eng = r.split(":")
         v, b = int(v), int(b)
+        b = b or n  # 0: b = n
         if n % b or not _lib.engine_supported(EQ_CODES[a.eq], n, b, v, eng):
             continue
         plan = executor.Plan(a.eq, ins, variant=v, b=b, engine=eng)
