@@ -390,6 +390,8 @@ int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int 
                                const double* const* inputs, double* X, int* info, void* stream, int engine,
                                unsigned long long* d_prof) {
   if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWSWEEP) return fail(LAGEN_EINVAL, "unknown engine");
+  if (eq < 0 || eq > 2) return fail(LAGEN_EINVAL, "unknown equation");
+  if (batch < 0) return fail(LAGEN_EINVAL, "negative batch");
   int rc = validate(eq, stmts, nstmts);
   if (rc) return rc;
   // engines with their own instance for (n, b) that the generic table lacks
@@ -601,6 +603,8 @@ int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, 
 int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                    const double* const* h_inputs, double* h_X, int* h_info, int engine) {
   if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWSWEEP) return fail(LAGEN_EINVAL, "unknown engine");
+  if (eq < 0 || eq > 2) return fail(LAGEN_EINVAL, "unknown equation");
+  if (batch < 0) return fail(LAGEN_EINVAL, "negative batch");
   int rc = validate(eq, stmts, nstmts);
   if (rc) return rc;
   // engines with their own instance for (n, b) that the generic table lacks

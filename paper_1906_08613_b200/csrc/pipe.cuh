@@ -272,22 +272,104 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
     });
   };
 
-  // updater step d, phase CRIT (the warp's tiles on diagonal d: their last
-  // contributions, then the right-hand side to the solve scratch) or BULK
-  // (every later tile of the warp's columns); both take diagonal d-1's
-  // contributions
-  auto upd_phase = [&](int d, bool crit, double (&a0)[NSLOT], double (&a1)[NSLOT]) {
+  // updater step d: diagonal d-1's contributions into the warp's tiles —
+  // phase CRIT: the tile of each column on diagonal d, then its right-hand
+  // side to the solve scratch; phase BULK: every later tile.  The active tiles
+  // of a column are a contiguous row range, entered through a switch whose
+  // cases fall through (static register slots, no per-tile tests beyond the
+  // range end): L X into rows [lo, hi], X U into rows [lo, min(hi, d-1)].
+  auto slotof = [&](int u, int I) { return FOLD ? (u == 0 ? I : T - I) : u * T + I; };
+  auto colJ = [&](int u) { return FOLD ? (u == 0 ? w : T - 1 - w) : colof(u); };
+  constexpr int NCOL = FOLD ? 2 : CU;
+  auto tile_lx = [&](const Pre& q, int I, double& c0, double& c1) {
+    const double* A = q.pL + ltidx(I, 0) * 64;
+    dmma(c0, c1, A[oA0], q.b0);
+    dmma(c0, c1, A[oA1], q.b1);
+  };
+  auto tile_xu = [&](int d, const Pre& q, const double* pv, int I, double& c0, double& c1) {
+    const double* B = q.pU - I * 64;
+    if constexpr (EQ == 2) {
+      const double* A = pv + I * PS;
+      dmma(c0, c1, A[oA0], B[oB0]);
+      dmma(c0, c1, A[oA1], B[oB1]);
+    } else {  // X_Ik: upper tile (I, k) or (k, I)^T;  U_kJ = L_Jk^T
+      const int kp = d - 1 - I;
+      const bool up = I <= kp;
+      const double* A = pv + (up ? I : kp) * PS;
+      dmma(c0, c1, A[up ? oA0 : oB0], B[oA0]);
+      dmma(c0, c1, A[up ? oA1 : oB1], B[oA1]);
+    }
+  };
+#define PIPE_I16(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15)
+  auto upd_crit = [&](int d, double (&a0)[NSLOT], double (&a1)[NSLOT]) {
     const double* pv = dbuf(d - 1);
     const int i0 = i0of(d);
-    constexpr int NPRE = FOLD ? 2 : CU;
-    Pre pre[NPRE];
 #pragma unroll
-    for (int u = 0; u < NPRE; ++u) pre[u] = prep(d, FOLD ? (u ? T - 1 - w : w) : colof(u), pv);
-    for_slots([&](int f, int I, int J, int u) {
-      if (crit ? I + J != d : I + J <= d) return;
-      tile_upd(d, pre[u], pv, I, a0[f], a1[f]);
-      if (crit) *reinterpret_cast<double2*>(Skb + (I - i0) * QP + oR) = make_double2(a0[f], a1[f]);
-    });
+    for (int u = 0; u < NCOL; ++u) {
+      const int J = colJ(u);
+      if (J >= T || (FOLD && u == 1 && J <= w)) continue;
+      const int hi = EQ == 2 ? T - 1 : J;
+      const int Ic = d - J;
+      if (Ic < 0 || Ic > hi) continue;
+      const Pre q = prep(d, J, pv);
+      switch (Ic) {
+#define PIPE_CRIT(i)                                                                  \
+  case i:                                                                             \
+    if constexpr (i < T) {                                                            \
+      const int f = slotof(u, i);                                                     \
+      if (q.lx) tile_lx(q, i, a0[f], a1[f]);                                          \
+      if (J >= 1) tile_xu(d, q, pv, i, a0[f], a1[f]);                                 \
+      *reinterpret_cast<double2*>(Skb + (i - i0) * QP + oR) = make_double2(a0[f], a1[f]); \
+    }                                                                                 \
+    break;
+        PIPE_I16(PIPE_CRIT)
+#undef PIPE_CRIT
+        default: break;
+      }
+    }
+  };
+  auto upd_bulk = [&](int d, double (&a0)[NSLOT], double (&a1)[NSLOT]) {
+    const double* pv = dbuf(d - 1);
+#pragma unroll
+    for (int u = 0; u < NCOL; ++u) {
+      const int J = colJ(u);
+      if (J >= T || (FOLD && u == 1 && J <= w)) continue;
+      const int hi = EQ == 2 ? T - 1 : J;
+      const int lo = d + 1 - J > 0 ? d + 1 - J : 0;
+      if (lo > hi) continue;
+      const Pre q = prep(d, J, pv);
+      if (q.lx) {
+        switch (lo) {
+#define PIPE_LX(i)                        \
+  case i:                                 \
+    if constexpr (i < T) {                \
+      if (i > hi) break;                  \
+      const int f = slotof(u, i);         \
+      tile_lx(q, i, a0[f], a1[f]);        \
+    }                                     \
+    [[fallthrough]];
+          PIPE_I16(PIPE_LX)
+#undef PIPE_LX
+          default: break;
+        }
+      }
+      const int hx = hi < d - 1 ? hi : d - 1;
+      if (lo <= hx) {
+        switch (lo) {
+#define PIPE_XU(i)                         \
+  case i:                                  \
+    if constexpr (i < T) {                 \
+      if (i > hx) break;                   \
+      const int f = slotof(u, i);          \
+      tile_xu(d, q, pv, i, a0[f], a1[f]);  \
+    }                                      \
+    [[fallthrough]];
+          PIPE_I16(PIPE_XU)
+#undef PIPE_XU
+          default: break;
+        }
+      }
+    }
   };
 
   // solver step d (d = -1: build Lsh): tile i = 4 sv + q of diagonal d, in
@@ -479,14 +561,14 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
 #pragma unroll 1
       for (int d = 0; d <= 2 * T - 2; ++d) {
         if (w == 0) stamp(256 + 2 * (d + 1));
-        upd_phase(d, true, a0, a1);
+        upd_crit(d, a0, a1);
         if constexpr (MODE == 0) {
           asm volatile("bar.arrive 2, %0;" ::"n"(P::THREADS) : "memory");
         } else {
           __syncwarp();
           sol_step(d, prob, bad);
         }
-        upd_phase(d, false, a0, a1);
+        upd_bulk(d, a0, a1);
         if (w == 0) stamp(256 + 2 * (d + 1) + 1);
         gbar();
       }

@@ -6,6 +6,8 @@ import pytest
 
 REPO = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(REPO))
+sys.path.insert(0, str(REPO / "tests"))  # test helpers (large_golden)
+TESTS_DIR = REPO / "tests"
 # the reference frontend, when installed beside the repo (baseline/_ref) or
 # present in this container; never required by the -m gpu parity tests
 for cand in (REPO / "baseline" / "_ref", Path("/root/reference/pkg/src")):

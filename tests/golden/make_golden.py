@@ -6,6 +6,8 @@ Run in the build container, where the reference package is importable:
 
 For every equation, n in SIZES, every synthesised variant and every default
 block size b (cli.default_blocks, /root/reference/pkg/src/lagen/cli.py:89-93)
+plus b = n (one block: the leaf kernel on the whole matrix, admissible for
+interpret_algorithm, verify.py:232-233)
 it records the reference executor's output
 (`interpret_algorithm`, /root/reference/pkg/src/lagen/verify.py:221-303) and
 dynamic flop count on two instances:
@@ -62,7 +64,7 @@ def main():
                 if n <= 16:
                     data[f"oracle_{case}_{n}"] = oracle_solve(inst)["X"]
                 for alg in algs:
-                    for b in default_blocks(n):
+                    for b in sorted(set(default_blocks(n)) | {n}):
                         out, flops = interpret_algorithm(alg, inst, b)
                         key = f"x_{case}_{n}_v{alg.index}_b{b}"
                         data[key] = out["X"]

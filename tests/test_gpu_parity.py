@@ -1,10 +1,14 @@
 """GPU parity: the CUDA path (through the C ABI) against the reference.
 
   * golden vectors of the reference's interpret_algorithm, every variant,
-    every default b, n in {4, 8, 12, 16, 24, 32}, two instance families;
+    every default b and b = n, n in {4, 8, 12, 16, 24, 32}, two instance
+    families; and projections of the reference's outputs at n in
+    {48, 64, 96, 128}, every variant x default b (make_golden_large.py);
+    every engine against the SAME (variant, b)'s reference output;
   * the CPU oracle (oracle/lagen_oracle.c, pinned to the reference by
     test_oracle_golden.py) on device-generated BASELINE inputs, every
-    variant x b at every n in 4..128;
+    variant x b x engine at every n in 4..128 against the oracle's run of
+    the same variant and b;
   * size-independent properties at full BASELINE batch sizes (residual,
     exact structure, shard invariance, host pipeline == device path).
 
@@ -37,6 +41,21 @@ def _cuda():
     torch.cuda.set_device(0)
 
 
+# every engine of the C ABI (LAGEN_ENGINE_*), auto excluded
+ENGINES = ("generic", "warp", "column", "dataflow", "rows", "wave", "rowspad", "pipe", "rowsweep")
+
+
+def blocks_of(n):
+    """the reference's default blocks plus b = n (verify.py:232-233)"""
+    return sorted(set(default_blocks(n)) | {n})
+
+
+def engine_runs(eq, n, variants, blocks=None):
+    from paper_1906_08613_b200 import _lib
+    return [(v, b, e) for e in ENGINES for v in variants for b in (blocks or blocks_of(n))
+            if _lib.engine_supported(EQ_CODES[eq], n, b, v, e)]
+
+
 def rel_diff(X, Y):
     num = np.linalg.norm((X - Y).reshape(X.shape[0], -1), axis=1)
     den = np.maximum(1.0, np.linalg.norm(Y.reshape(Y.shape[0], -1), axis=1))
@@ -55,11 +74,8 @@ def test_golden_reference_vectors(eq):
     groups = {}
     for e in META[eq]["entries"]:
         groups.setdefault((e["n"], e["variant"], e["b"]), []).append(e)
-    from paper_1906_08613_b200 import _lib
     for (n, v, b), es in groups.items():
-      for engine in ("generic", "warp", "column", "dataflow", "rows", "wave", "rowspad"):
-        if not _lib.engine_supported(EQ_CODES[eq], n, b, v, engine):
-            continue
+      for _, _, engine in engine_runs(eq, n, [v], [b]):
         ins = [np.stack([d[f"in_{e['case']}_{n}_{nm}"] for e in es]) for nm in EQ_INPUTS[eq]]
         X, info = executor.solve(eq, to_dev(ins), variant=v, b=b, engine=engine)
         X = X.cpu().numpy()
@@ -67,7 +83,7 @@ def test_golden_reference_vectors(eq):
         assert (info.cpu().numpy() == 0).all()
         err = rel_diff(X, want).max()
         worst = max(worst, err)
-        assert err <= REL_TOL, (eq, n, v, b, err)
+        assert err <= REL_TOL, (eq, n, v, b, engine, err)
         if eq == "cholesky":
             assert np.all(np.tril(X, -1) == 0.0)
         if eq == "lyapunov":
@@ -85,25 +101,69 @@ def test_every_variant_vs_oracle(eq, n, oracle_mod):
     ins_d = executor.generate(eq, n, seed=n, batch=batch)
     ins_h = [t.cpu().numpy() for t in ins_d]
     vs = builtin_variants(eq)
-    ref_X, ref_info = oracle_mod.execute(eq, vs[0].statements, n, default_blocks(n)[0], ins_h)
-    assert (ref_info == 0).all()
     res_tol = 10 * n * EPS
-    from paper_1906_08613_b200 import _lib
-    runs = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows", "wave", "rowspad") for v in vs for b in default_blocks(n)
-            if _lib.engine_supported(EQ_CODES[eq], n, b, v.index, e)]
-    for v, b, engine in runs:
-        if True:
-            X, info = executor.solve(eq, ins_d, variant=v.index, b=b, engine=engine)
-            X = X.cpu().numpy()
-            assert (info.cpu().numpy() == 0).all(), (eq, n, v.index, b, engine)
-            err = rel_diff(X, ref_X).max()
-            assert err <= REL_TOL, (eq, n, v.index, b, engine, err)
-            res = oracle_mod.residual(eq, n, ins_h, X)
-            assert res.max() <= res_tol, (eq, n, v.index, b, engine, res.max() / (n * EPS))
-            if eq == "cholesky":
-                assert np.all(np.tril(X, -1) == 0.0)
-            if eq == "lyapunov":
-                assert np.array_equal(X, np.transpose(X, (0, 2, 1)))
+    refs = {}
+    for v, b, engine in engine_runs(eq, n, [v.index for v in vs]):
+        if (v, b) not in refs:  # the oracle's run of the same variant and block size
+            ref_X, ref_info = oracle_mod.execute(eq, vs[v].statements, n, b, ins_h)
+            assert (ref_info == 0).all()
+            refs[(v, b)] = ref_X
+        ref_X = refs[(v, b)]
+        X, info = executor.solve(eq, ins_d, variant=v, b=b, engine=engine)
+        X = X.cpu().numpy()
+        assert (info.cpu().numpy() == 0).all(), (eq, n, v, b, engine)
+        err = rel_diff(X, ref_X).max()
+        assert err <= REL_TOL, (eq, n, v, b, engine, err)
+        res = oracle_mod.residual(eq, n, ins_h, X)
+        assert res.max() <= res_tol, (eq, n, v, b, engine, res.max() / (n * EPS))
+        if eq == "cholesky":
+            assert np.all(np.tril(X, -1) == 0.0)
+        if eq == "lyapunov":
+            assert np.array_equal(X, np.transpose(X, (0, 2, 1)))
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+def test_large_n_reference_goldens(eq, oracle_mod):
+    """n = 48, 64, 96, 128: every engine x variant x default b against the
+    reference interpreter's own output for the same (variant, b), through
+    its projections (tests/golden/make_golden_large.py)."""
+    import large_golden as lg
+    d = lg.data(eq)
+    cache = {}
+    worst = 0.0
+    for (n, v, b), es in lg.groups(eq).items():
+        if n not in cache:
+            cache[n] = to_dev(lg.inputs(oracle_mod, eq, n, d))
+        for _, _, engine in engine_runs(eq, n, [v], [b]):
+            X, info = executor.solve(eq, cache[n], variant=v, b=b, engine=engine)
+            assert (info.cpu().numpy() == 0).all(), (eq, n, v, b, engine)
+            err = lg.max_rel_err(X.cpu().numpy(), d, es)
+            worst = max(worst, err)
+            assert err <= REL_TOL, (eq, n, v, b, engine, err)
+    print(f"{eq}: worst projected relative difference vs reference at n >= 48: {worst:.3e}")
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+@pytest.mark.parametrize("n", [12, 16, 64, 124])
+def test_every_engine_multi_round(eq, n, oracle_mod):
+    """Batches larger than one round of resident problem slots, with a
+    partial last round: every engine's loop-carried path (persistent CTAs,
+    prefetch, slot reuse) against the oracle on the first and last problems."""
+    batch = {12: 40001, 16: 30001, 64: 4001, 124: 1201}[n]
+    ins_d = executor.generate(eq, n, seed=5 * n, batch=batch)
+    pick = np.r_[0:16, batch - 16:batch]
+    sub = [t[pick].cpu().numpy() for t in ins_d]
+    vs = builtin_variants(eq)
+    seen = set()
+    for v, b, engine in engine_runs(eq, n, [v.index for v in vs]):
+        if (engine, b) in seen:  # one variant per engine and block size keeps this test short
+            continue
+        seen.add((engine, b))
+        X, info = executor.solve(eq, ins_d, variant=v, b=b, engine=engine)
+        assert int((info != 0).sum()) == 0, (eq, n, v, b, engine)
+        ref, _ = oracle_mod.execute(eq, vs[v].statements, n, b, sub)
+        err = rel_diff(X[torch.from_numpy(pick).cuda()].cpu().numpy(), ref).max()
+        assert err <= REL_TOL, (eq, n, v, b, engine, err)
 
 
 ODD_N = [1, 2, 3, 5, 6, 7, 9, 10, 13, 18, 30, 31, 33, 47, 63, 66, 97, 127]
@@ -170,7 +230,7 @@ def test_non_spd_and_nan_are_reported():
     """info = first non-positive pivot + 1 (kernels.py:87-88) / -1 for NaN-Inf,
     on every engine that has the variant."""
     from paper_1906_08613_b200 import _lib
-    for n, bad in ((16, 6), (48, 37)):
+    for n, bad in ((16, 6), (32, 20), (48, 37)):
         A = executor.generate("cholesky", n, seed=1, batch=4)[0]
         A[2, bad, bad] = -1000.0
         with pytest.raises(errors.VerificationError):
@@ -183,18 +243,20 @@ def test_non_spd_and_nan_are_reported():
                 assert info.cpu().tolist() == [0, 0, bad + 1, 0], (n, v, engine)
         L, U, C = executor.generate("sylvester", n, seed=1, batch=3)
         C[1, 0, 0] = float("nan")
-        for engine in ("generic", "warp", "dataflow", "wave"):
-            if not _lib.engine_supported(2, n, 4, 13, engine):
-                continue
-            _, info = executor.solve("sylvester", [L, U, C], variant=13, b=4, check=False, engine=engine)
-            assert info.cpu().tolist() == [0, -1, 0], (n, engine)
+        for engine in ENGINES:
+            for b in (4, n):
+                if not _lib.engine_supported(2, n, b, 13, engine):
+                    continue
+                _, info = executor.solve("sylvester", [L, U, C], variant=13, b=b, check=False, engine=engine)
+                assert info.cpu().tolist() == [0, -1, 0], (n, b, engine)
         L, S = executor.generate("lyapunov", n, seed=1, batch=3)
         S[2, n - 1, n - 1] = float("inf")
-        for engine in ("generic", "warp", "dataflow", "wave"):
-            if not _lib.engine_supported(1, n, 4, 5, engine):
-                continue
-            _, info = executor.solve("lyapunov", [L, S], variant=5, b=4, check=False, engine=engine)
-            assert info.cpu().tolist() == [0, 0, -1], (n, engine)
+        for engine in ENGINES:
+            for b in (4, n):
+                if not _lib.engine_supported(1, n, b, 5, engine):
+                    continue
+                _, info = executor.solve("lyapunov", [L, S], variant=5, b=b, check=False, engine=engine)
+                assert info.cpu().tolist() == [0, 0, -1], (n, b, engine)
     try:
         import lagen.errors
         with pytest.raises(lagen.errors.VerificationError):
@@ -299,3 +361,84 @@ def test_reference_algorithm_objects_drop_in():
                 assert gflops == wflops
                 x = want["X"]
                 assert np.linalg.norm(got["X"] - x) <= REL_TOL * max(1.0, np.linalg.norm(x))
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+def test_config5_sampled(eq, oracle_mod):
+    """BASELINE config 5 on one GPU: n = 64, 2^20 problems (2^32 doubles per
+    operand, past the 2^31-element line), seed 7; every problem's info, the
+    last 64 problems (largest offsets) and 64 spread ones against the oracle."""
+    n, batch = 64, 1 << 20
+    ins = executor.generate(eq, n, seed=7, batch=batch)
+    X, info = executor.solve(eq, ins, check=False)
+    assert int((info != 0).sum()) == 0
+    pick = np.r_[np.linspace(0, batch - 65, 64).astype(np.int64), batch - 64:batch]
+    idx = torch.from_numpy(pick).cuda()
+    sub = [t[idx].cpu().numpy() for t in ins]
+    from paper_1906_08613_b200 import dispatch
+    sel = dispatch.select(eq, n)
+    ref, rinfo = oracle_mod.execute(eq, builtin_variants(eq)[sel["variant"]].statements, n,
+                                    sel["b"] if n % sel["b"] == 0 else default_blocks(n)[0], sub)
+    assert (rinfo == 0).all()
+    assert rel_diff(X[idx].cpu().numpy(), ref).max() <= REL_TOL
+    # the generator is index-keyed: the last problems equal a fresh generation at their offset
+    tail = executor.generate(eq, n, seed=7, batch=64, first=batch - 64)
+    for a, b in zip(ins, tail):
+        assert torch.equal(a[batch - 64:], b)
+    del ins, X
+    torch.cuda.empty_cache()
+
+
+def test_typed_entry_points_against_goldens():
+    """lagen_b200_cholesky / _lyapunov / _sylvester — the replacements of the
+    emitted kernel <eq>_v<k>_n<n>_b<b>(inputs..., X) (codegen.py:143-201) —
+    called through ctypes on the reference's golden inputs."""
+    import ctypes
+    from paper_1906_08613_b200 import _lib
+    fns = {"cholesky": _lib.lib.lagen_b200_cholesky, "lyapunov": _lib.lib.lagen_b200_lyapunov,
+           "sylvester": _lib.lib.lagen_b200_sylvester}
+    for eq in EQUATIONS:
+        d = np.load(GOLDEN / f"{eq}.npz")
+        for e in META[eq]["entries"]:
+            if e["case"] != "base" or e["n"] not in (8, 24, 32):
+                continue
+            n = e["n"]
+            ins = to_dev([d[f"in_base_{n}_{nm}"][None] for nm in EQ_INPUTS[eq]])
+            X = torch.full((1, n, n), float("nan"), dtype=torch.float64, device="cuda")  # every entry is written
+            info = torch.full((1,), 7, dtype=torch.int32, device="cuda")
+            ptrs = [ctypes.c_void_p(t.data_ptr()) for t in ins]
+            rc = fns[eq](e["variant"], n, e["b"], 1, *ptrs, ctypes.c_void_p(X.data_ptr()),
+                         ctypes.c_void_p(info.data_ptr()), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+            assert rc == 0, _lib.lib.lagen_b200_last_error()
+            torch.cuda.synchronize()
+            assert int(info[0]) == 0
+            want = d[e["key"]][None]
+            assert rel_diff(X.cpu().numpy(), want).max() <= REL_TOL, (eq, e["key"])
+    # errors come back as status codes, not exceptions
+    A = torch.zeros((1, 8, 8), dtype=torch.float64, device="cuda")
+    assert _lib.lib.lagen_b200_cholesky(0, 8, 3, 1, ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(A.data_ptr()),
+                                        None, None) == -2
+    assert _lib.lib.lagen_b200_cholesky(99, 8, 4, 1, ctypes.c_void_p(A.data_ptr()), ctypes.c_void_p(A.data_ptr()),
+                                        None, None) == -3
+
+
+@pytest.mark.parametrize("eq", ["lyapunov", "sylvester"])
+def test_padded_sizes_with_minus_one_diagonal(eq, oracle_mod):
+    """n not a multiple of 4 runs identity-padded in the C ABI; a real
+    diagonal entry of -1 must not meet a padded pivot of +1 (0 / 0): the pad
+    value is 1 + max |diagonal| per problem."""
+    for n in (6, 30):
+        ins = executor.generate(eq, n, seed=3, batch=4)
+        # well-conditioned pivots around the -1 entries: the other diagonal
+        # entries of those problems are 3 (pivots -1 + 3, 3 + 3, -1 - 1)
+        for p, (op, k) in ((1, (0, 2)), (2, (1 if eq == "sylvester" else 0, n - 1))):
+            for t in ins[:-1]:
+                t[p].diagonal().fill_(3.0)
+            ins[op][p, k, k] = -1.0
+        ins_h = [t.cpu().numpy() for t in ins]
+        for v in (0, len(builtin_variants(eq)) - 1):
+            for b in sorted({1, 2, n} & {d for d in range(1, n + 1) if n % d == 0}):
+                X, info = executor.solve(eq, ins, variant=v, b=b, check=False)
+                assert info.cpu().tolist() == [0, 0, 0, 0], (eq, n, v, b)
+                ref, _ = oracle_mod.execute(eq, builtin_variants(eq)[v].statements, n, b, ins_h)
+                assert rel_diff(X.cpu().numpy(), ref).max() <= REL_TOL

@@ -154,3 +154,21 @@ def test_compulsory_bytes_model():
         assert bytes_compulsory("cholesky", n) == 12 * n * n + 4 * n
         assert bytes_compulsory("lyapunov", n) == 16 * n * n + 8 * n
         assert bytes_compulsory("sylvester", n) == 24 * n * n + 8 * n
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+def test_oracle_matches_reference_large_n(eq, oracle_mod):
+    """n = 48 ... 128, every variant x default b, against the reference
+    interpreter's projections (tests/golden/make_golden_large.py)."""
+    import large_golden as lg
+    d = lg.data(eq)
+    vs = builtin_variants(eq)
+    worst = 0.0
+    cache = {}
+    for (n, v, b), es in lg.groups(eq).items():
+        if n not in cache:
+            cache[n] = lg.inputs(oracle_mod, eq, n, d)
+        X, info = oracle_mod.execute(eq, vs[v].statements, n, b, cache[n])
+        assert (info == 0).all()
+        worst = max(worst, lg.max_rel_err(X, d, es))
+    assert worst <= 1e-13, worst

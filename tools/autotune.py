@@ -57,9 +57,14 @@ def main():
             rows = []
             ref_X = None
             from paper_1906_08613_b200 import _lib
-            cands = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows", "wave", "rowspad")
-                     for v in builtin_variants(eq) for b in default_blocks(n)
-                     if _lib.engine_supported(_lib_eq(eq), n, b, v.index, e)]
+            # the reference's default blocks plus b = n (admissible: verify.py:232-233)
+            blocks = sorted(set(default_blocks(n)) | {n})
+            cands = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows", "wave", "rowspad",
+                                         "pipe", "rowsweep")
+                     for v in builtin_variants(eq) for b in blocks
+                     if _lib.engine_supported(_lib_eq(eq), n, b, v.index, e)
+                     # rowsweep runs the same kernel for every variant (b = n): time one
+                     and not (e == "rowsweep" and v.index != {"lyapunov": 5, "sylvester": 13}.get(eq))]
             if args.engines != "all":
                 cands = [c for c in cands if c[2] in args.engines.split(",")]
             for v, b, engine in cands:
