@@ -173,6 +173,23 @@ int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, 
                                    long long batch, const double* const* h_inputs,
                                    double* h_X, int* h_info, int engine);
 
+/* Same with flags:
+ *   LAGEN_HOST_TRIANGLES: move only the structurally needed part of every
+ *     operand over PCIe — zero-copy kernels read A / S / U's upper and L's
+ *     lower triangles (rows rounded to 8-column tiles) straight from mapped
+ *     pinned host memory and write X back the same way.  Needs pinned
+ *     (cudaHostAlloc / cudaHostRegister-mapped) buffers and an even n.
+ *   LAGEN_HOST_X_ZEROED: the caller's X already holds zeros in its
+ *     structurally-zero part (the reference's contract: "outputs must be
+ *     zero-initialised by the caller", codegen.py:4-7); Cholesky then writes
+ *     only X's upper triangle. */
+#define LAGEN_HOST_TRIANGLES 1
+#define LAGEN_HOST_X_ZEROED 2
+int lagen_b200_execute_host_flags(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
+                                  long long batch, const double* const* h_inputs,
+                                  double* h_X, int* h_info, int engine, int flags);
+int lagen_b200_host_bytes_flags(int eq, int n, long long batch, int flags, long long* h2d, long long* d2h);
+
 /* Bytes the host pipeline moves per call (H2D of all inputs, D2H of X and
  * info).  With LAGEN_HOST_BANDS=1 (opt-in, measured not faster) Cholesky
  * n >= 32 copies only row bands of the upper triangle and zero-fills the rest

@@ -47,6 +47,8 @@ def _load():
     lib.lagen_b200_execute_host_engine.argtypes = [i, vp, i, i, i, ll, vp, vp, vp, i]
     lib.lagen_b200_generate.argtypes = [i, i, ctypes.c_ulonglong, ll, ll, vp, vp]
     lib.lagen_b200_host_bytes.argtypes = [i, i, ll, vp, vp]
+    lib.lagen_b200_execute_host_flags.argtypes = [i, vp, i, i, i, ll, vp, vp, vp, i, i]
+    lib.lagen_b200_host_bytes_flags.argtypes = [i, i, ll, i, vp, vp]
     lib.lagen_b200_cholesky.argtypes = [i, i, i, ll, vp, vp, vp, vp]
     lib.lagen_b200_lyapunov.argtypes = [i, i, i, ll, vp, vp, vp, vp, vp]
     lib.lagen_b200_sylvester.argtypes = [i, i, i, ll, vp, vp, vp, vp, vp, vp]
@@ -62,15 +64,19 @@ EXPORTED = (
     "lagen_b200_cholesky", "lagen_b200_lyapunov", "lagen_b200_sylvester",
     "lagen_b200_execute", "lagen_b200_execute_host", "lagen_b200_execute_host_engine", "lagen_b200_generate",
     "lagen_b200_execute_engine", "lagen_b200_warp_supported", "lagen_b200_engine_supported",
-    "lagen_b200_execute_profile", "lagen_b200_host_bytes",
+    "lagen_b200_execute_profile", "lagen_b200_host_bytes", "lagen_b200_execute_host_flags",
+    "lagen_b200_host_bytes_flags",
 )
+HOST_TRIANGLES = 1
+HOST_X_ZEROED = 2
 ENGINES = {"auto": 0, "generic": 1, "warp": 2, "column": 3, "dataflow": 4, "rows": 5, "wave": 6, "rowspad": 7, "pipe": 8, "rowsweep": 9}
 
 
-def host_bytes(eq_code, n, batch):
+def host_bytes(eq_code, n, batch, flags=0):
     """(H2D, D2H) bytes one host-pipeline call moves over PCIe."""
     h2d, d2h = ctypes.c_longlong(0), ctypes.c_longlong(0)
-    check(lib.lagen_b200_host_bytes(eq_code, n, batch, ctypes.byref(h2d), ctypes.byref(d2h)), "host_bytes")
+    check(lib.lagen_b200_host_bytes_flags(eq_code, n, batch, flags, ctypes.byref(h2d), ctypes.byref(d2h)),
+          "host_bytes")
     return h2d.value, d2h.value
 
 

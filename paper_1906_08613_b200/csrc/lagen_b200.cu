@@ -580,7 +580,10 @@ struct HostPipe {
     cudaError_t err = cudaSuccess;
     for (int k = 0; k < kNS && err == cudaSuccess; ++k) {
       if (!st[k]) err = cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
-      for (int i = 0; i < 3 && err == cudaSuccess; ++i) err = cudaMalloc(&d_in[k][i], bytes);
+      for (int i = 0; i < 3 && err == cudaSuccess; ++i) {
+        err = cudaMalloc(&d_in[k][i], bytes);
+        if (err == cudaSuccess) err = cudaMemset(d_in[k][i], 0, bytes);  // never-copied parts read as 0
+      }
       if (err == cudaSuccess) err = cudaMalloc(&d_X[k], bytes);
       if (err == cudaSuccess) err = cudaMalloc(&d_info[k], info_bytes);
     }
@@ -593,6 +596,82 @@ struct HostPipe {
 };
 std::mutex g_pipe_mu;
 HostPipe g_pipe[64];
+
+// Zero-copy triangle transfer (LAGEN_HOST_TRIANGLES): kernels read the
+// needed part of each input row straight from mapped pinned host memory into
+// the device staging buffer, and write X's rows back the same way, so PCIe
+// carries only the structurally needed bytes (SURVEY §8d compulsory bytes)
+// instead of dense matrices.  Row r of an operand moves columns [c0, c1):
+//   part 0 (full)  : [0, n)
+//   part 1 (upper) : [8 floor(r / 8), n)      A, S, U; Cholesky X (zeroed host X)
+//   part 2 (lower) : [0, min(n, 8 floor(r / 8) + 8))   L
+// in 16-byte units (n even).  The parts of the device staging buffer that are
+// not copied hold stale finite values (zeroed on allocation); no engine reads
+// them (tests: test_unread_triangles_are_ignored).
+__host__ __device__ inline void part_cols(int part, int n, int r, int* c0, int* c1) {
+  *c0 = part == 1 ? (r & ~7) : 0;
+  *c1 = part == 2 ? ((r & ~7) + 8 < n ? (r & ~7) + 8 : n) : n;
+}
+// rows' 16-byte unit offsets inside one problem: unit u of the problem lies in
+// row r with start[r] <= u < start[r + 1], column col0[r] + 2 (u - start[r])
+struct TriRows {
+  int start[130];
+  int col0[129];
+};
+__global__ void tri_copy_kernel(const double* __restrict__ src, double* __restrict__ dst, long long cnt, int n,
+                                const __grid_constant__ TriRows tr) {
+  const int U = tr.start[n];  // units per problem
+  const long long total = cnt * U;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += stride) {
+    const long long p = i / U;
+    const int u = (int)(i - p * U);
+    int lo = 0, hi = n - 1;  // last row with start <= u
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tr.start[mid] <= u) lo = mid;
+      else hi = mid - 1;
+    }
+    const long long off = (p * n + lo) * n + tr.col0[lo] + 2 * (u - tr.start[lo]);
+    *reinterpret_cast<double2*>(dst + off) = *reinterpret_cast<const double2*>(src + off);
+  }
+}
+TriRows tri_rows(int part, int n) {
+  TriRows t;
+  t.start[0] = 0;
+  for (int r = 0; r < n; ++r) {
+    int c0, c1;
+    part_cols(part, n, r, &c0, &c1);
+    t.col0[r] = c0;
+    t.start[r + 1] = t.start[r] + (c1 - c0) / 2;
+  }
+  return t;
+}
+int input_part(int eq, int i) {
+  if (eq == LAGEN_CHOLESKY) return 1;                 // A: upper
+  if (i == 0) return 2;                               // L: lower
+  if (eq == LAGEN_LYAPUNOV) return 1;                 // S: upper
+  return i == 1 ? 1 : 0;                              // Sylvester U: upper, C: full
+}
+long long part_doubles(int part, int n) {
+  long long t = 0;
+  for (int r = 0; r < n; ++r) {
+    int c0, c1;
+    part_cols(part, n, r, &c0, &c1);
+    t += c1 - c0;
+  }
+  return t;
+}
+// device address of mapped pinned host memory, or nullptr
+const void* mapped(const void* h) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+  return a.devicePointer;
+}
 }  // namespace
 
 int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
@@ -602,6 +681,12 @@ int lagen_b200_execute_host(int eq, const lagen_stmt* stmts, int nstmts, int n, 
 
 int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                    const double* const* h_inputs, double* h_X, int* h_info, int engine) {
+  return lagen_b200_execute_host_flags(eq, stmts, nstmts, n, b, batch, h_inputs, h_X, h_info, engine, 0);
+}
+
+int lagen_b200_execute_host_flags(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
+                                  const double* const* h_inputs, double* h_X, int* h_info, int engine, int flags) {
+  if (flags & ~(LAGEN_HOST_TRIANGLES | LAGEN_HOST_X_ZEROED)) return fail(LAGEN_EINVAL, "unknown host flags");
   if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWSWEEP) return fail(LAGEN_EINVAL, "unknown engine");
   if (eq < 0 || eq > 2) return fail(LAGEN_EINVAL, "unknown equation");
   if (batch < 0) return fail(LAGEN_EINVAL, "negative batch");
@@ -634,6 +719,51 @@ int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, 
   err = hp.reserve((size_t)chunk * prob_bytes, (size_t)chunk * sizeof(int));
   if (err != cudaSuccess) return cuda_fail(err, "host pipeline setup");
   if (chunk > batch) chunk = batch;
+  // zero-copy triangles: every buffer must be mapped pinned memory and n even
+  const double* mh_in[3] = {nullptr, nullptr, nullptr};
+  double* mh_X = nullptr;
+  bool tri = (flags & LAGEN_HOST_TRIANGLES) && n % 2 == 0;
+  for (int i = 0; i < nin && tri; ++i) tri = (mh_in[i] = static_cast<const double*>(mapped(h_inputs[i]))) != nullptr;
+  if (tri) tri = (mh_X = static_cast<double*>(const_cast<void*>(mapped(h_X)))) != nullptr;
+  if ((flags & LAGEN_HOST_TRIANGLES) && !tri)
+    return fail(LAGEN_EINVAL, "LAGEN_HOST_TRIANGLES needs mapped pinned host buffers and an even n");
+  const int xpart = (eq == LAGEN_CHOLESKY && (flags & LAGEN_HOST_X_ZEROED)) ? 1 : 0;
+  if (tri) {
+    int status = LAGEN_OK;
+    // the transfer kernels run on SMs the persistent solves leave free
+    struct Reserve {
+      Reserve() { t_sm_reserve = 8; }
+      ~Reserve() { t_sm_reserve = 0; }
+    } reserve_guard;
+    TriRows parts[3] = {tri_rows(0, n), tri_rows(1, n), tri_rows(2, n)};
+    auto tcopy = [&](const double* src, double* dst, long long cnt, int part, cudaStream_t st) {
+      const long long units = cnt * parts[part].start[n];
+      long long grid = (units + 511) / 512;
+      if (grid > 32) grid = 32;  // 32 CTAs x 512 threads keep PCIe busy (tools/zc_probe.cu)
+      tri_copy_kernel<<<(unsigned)grid, 512, 0, st>>>(src, dst, cnt, n, parts[part]);
+      return cudaGetLastError();
+    };
+    for (long long c0 = 0, it = 0; status == LAGEN_OK && c0 < batch; c0 += chunk, ++it) {
+      const int k = (int)(it % kNS);
+      const long long cnt = (batch - c0) < chunk ? (batch - c0) : chunk;
+      for (int i = 0; i < nin && err == cudaSuccess; ++i)
+        err = tcopy(mh_in[i] + c0 * n * n, hp.d_in[k][i], cnt, input_part(eq, i), hp.st[k]);
+      if (err != cudaSuccess) { status = cuda_fail(err, "triangle gather"); break; }
+      const double* ins[3] = {hp.d_in[k][0], hp.d_in[k][1], hp.d_in[k][2]};
+      status = lagen_b200_execute_engine(eq, stmts, nstmts, n, b, cnt, ins, hp.d_X[k],
+                                         h_info ? hp.d_info[k] : nullptr, hp.st[k], engine);
+      if (status != LAGEN_OK) break;
+      err = tcopy(hp.d_X[k], mh_X + c0 * n * n, cnt, xpart, hp.st[k]);
+      if (err == cudaSuccess && h_info)
+        err = cudaMemcpyAsync(h_info + c0, hp.d_info[k], cnt * sizeof(int), cudaMemcpyDeviceToHost, hp.st[k]);
+      if (err != cudaSuccess) { status = cuda_fail(err, "triangle scatter"); break; }
+    }
+    for (int k = 0; k < kNS; ++k) {
+      cudaError_t e2 = cudaStreamSynchronize(hp.st[k]);
+      if (e2 != cudaSuccess && status == LAGEN_OK) status = cuda_fail(e2, "host pipeline sync");
+    }
+    return status;
+  }
   // Cholesky: the strictly-lower part of X left of each band is zero; the
   // host writes it (threads, overlapped with the copies) instead of PCIe
   std::vector<std::thread> fill;
@@ -688,6 +818,17 @@ int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, 
   }
   for (auto& th : fill) th.join();
   return status;
+}
+
+int lagen_b200_host_bytes_flags(int eq, int n, long long batch, int flags, long long* h2d, long long* d2h) {
+  if (!(flags & LAGEN_HOST_TRIANGLES) || n % 2) return lagen_b200_host_bytes(eq, n, batch, h2d, d2h);
+  if (eq < 0 || eq > 2 || n < 1 || batch < 0) return fail(LAGEN_EINVAL, "bad arguments");
+  long long in = 0;
+  for (int i = 0; i < eq_ninputs(eq); ++i) in += part_doubles(input_part(eq, i), n);
+  const int xpart = (eq == LAGEN_CHOLESKY && (flags & LAGEN_HOST_X_ZEROED)) ? 1 : 0;
+  if (h2d) *h2d = batch * in * (long long)sizeof(double);
+  if (d2h) *d2h = batch * (part_doubles(xpart, n) * (long long)sizeof(double) + (long long)sizeof(int));
+  return LAGEN_OK;
 }
 
 int lagen_b200_host_bytes(int eq, int n, long long batch, long long* h2d, long long* d2h) {

@@ -20,6 +20,13 @@ struct LaunchArgs {
 
 typedef cudaError_t (*LaunchFn)(const LaunchArgs&, cudaStream_t);
 
+// SMs the persistent engines may fill (the calling thread's reservation, 0 by
+// default): the host pipeline leaves a few SMs to its zero-copy transfer
+// kernels, which otherwise could not start while a persistent solve holds
+// every SM
+inline thread_local int t_sm_reserve = 0;
+inline long long sm_budget(int sms) { return sms - t_sm_reserve < 1 ? 1 : sms - t_sm_reserve; }
+
 struct KernelEntry {
   int eq, n, b;
   int G, P, threads;

@@ -39,7 +39,7 @@ cudaError_t launch_col(const LaunchArgs& a, cudaStream_t s) {
   if (a.batch <= 0) return cudaSuccess;
   const long long per_cta = (long long)P::WARPS * P::GPW;
   const long long need = (a.batch + per_cta - 1) / per_cta;
-  const long long resident = (long long)ctas_per_sm.load() * sm_count.load();
+  const long long resident = (long long)ctas_per_sm.load() * sm_budget(sm_count.load());
   const long long grid = need < resident ? need : resident;
   kern<<<(unsigned)grid, P::WARPS * 32, P::SMEM, s>>>(a.in[0], a.X, a.info, a.batch);
   return cudaGetLastError();

@@ -142,7 +142,7 @@ cudaError_t launch_df(const LaunchArgs& a, cudaStream_t s) {
     }
   }
   if (a.batch <= 0) return cudaSuccess;
-  const long long resident = (long long)ctas_per_sm[dev] * sm_count[dev];
+  const long long resident = (long long)ctas_per_sm[dev] * sm_budget(sm_count[dev]);
   const long long grid = a.batch < resident ? a.batch : resident;
   kern<<<(unsigned)grid, P::THREADS, P::SMEM, s>>>(a.in[0], a.in[1], a.in[2], a.X, a.info, a.batch, sched[dev],
                                                    ntasks);

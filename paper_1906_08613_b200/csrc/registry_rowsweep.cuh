@@ -40,7 +40,7 @@ cudaError_t launch_rowsweep(const LaunchArgs& a, cudaStream_t s) {
   if (a.batch <= 0) return cudaSuccess;
   const long long per_cta = (long long)P::W * P::PPW;
   const long long need = (a.batch + per_cta - 1) / per_cta;
-  const long long resident = (long long)ctas_per_sm.load() * sm_count.load();
+  const long long resident = (long long)ctas_per_sm.load() * sm_budget(sm_count.load());
   const long long grid = need < resident ? need : resident;
   const double* L = a.in[0];
   const double* U = EQ == 2 ? a.in[1] : a.in[0];

@@ -41,7 +41,7 @@ cudaError_t launch_warp(const LaunchArgs& a, cudaStream_t s) {
   }
   if (a.batch <= 0) return cudaSuccess;
   const long long need = (a.batch + P::P - 1) / P::P;
-  const long long resident = (long long)ctas_per_sm.load() * sm_count.load();
+  const long long resident = (long long)ctas_per_sm.load() * sm_budget(sm_count.load());
   const long long grid = need < resident ? need : resident;
   kern<<<(unsigned)grid, P::WARPS * 32, P::SMEM, s>>>(a.in[0], a.in[1], a.in[2], a.X, a.info, a.batch, a.prof);
   return cudaGetLastError();

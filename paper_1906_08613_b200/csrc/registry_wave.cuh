@@ -92,7 +92,7 @@ cudaError_t launch_wave_cfg(const LaunchArgs& a, cudaStream_t s) {
   }
   if (a.batch <= 0) return cudaSuccess;
   const long long need = (a.batch + PP - 1) / PP;
-  const long long resident = (long long)ctas_per_sm.load() * sm_count.load();
+  const long long resident = (long long)ctas_per_sm.load() * sm_budget(sm_count.load());
   const long long grid = need < resident ? need : resident;
   // _signature order: lyapunov (L, S), sylvester (L, U, C)
   const double* L = a.in[0];

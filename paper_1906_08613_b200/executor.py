@@ -213,11 +213,24 @@ def interpret_algorithm(alg, inst, b, on_iteration=None):
     return {alg.output: X[0].cpu().numpy()}, flop_count(eq_name, stmts, n, b)
 
 
-def solve_host(eq, inputs, variant=None, b=None, out=None, info=None, engine=None):
+def solve_host(eq, inputs, variant=None, b=None, out=None, info=None, engine=None, triangles=None,
+               out_zeroed=False):
     """Host buffers (numpy arrays or CPU tensors, ideally pinned) -> host X.
-    Streams the batch through the GPU with H2D / solve / D2H overlap; runs the
-    same kernel as solve() (dispatch-table engine unless given)."""
+    Streams the batch through the GPU with transfer / solve overlap; runs the
+    same kernel as solve() (dispatch-table engine unless given).
+
+    triangles: move only the structurally needed part of each operand over
+    PCIe (zero-copy kernels on the mapped pinned buffers, LAGEN_HOST_TRIANGLES).
+    Zero-copy transfers reach ~37 GB/s each way against ~50 for the copy
+    engines' dense copies (tools/zc_probe.cu), so the default (None) uses them
+    only where the byte saving wins (tools/e2e_tri_probe.py): Cholesky with a
+    caller-zeroed X at n >= 48, Lyapunov at n >= 64; pinned buffers, even n.  out_zeroed: `out`
+    already holds zeros in X's structurally-zero part — the reference's own
+    contract for its emitted kernels (codegen.py:4-7) — so Cholesky writes
+    only X's upper triangle (LAGEN_HOST_X_ZEROED)."""
     eq_name = _eq_name(eq)
+    if out_zeroed and out is None:
+        raise errors.UsageError("out_zeroed needs a caller-provided out buffer")
     names = EQ_INPUTS[eq_name]
     if len(inputs) != len(names):
         raise errors.UsageError(f"{eq_name} takes inputs {names}, got {len(inputs)} arrays")
@@ -250,9 +263,13 @@ def solve_host(eq, inputs, variant=None, b=None, out=None, info=None, engine=Non
         raise errors.UsageError(f"info must be a contiguous int32 CPU tensor with >= {batch} entries")
     arr = _lib.stmt_array(stmts)
     ptrs = (ctypes.c_void_p * 3)(*([t.data_ptr() for t in arrs] + [0] * (3 - len(arrs))))
-    rc = _lib.lib.lagen_b200_execute_host_engine(EQ_CODES[eq_name], ctypes.addressof(arr), len(stmts), n, b,
-                                                 batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
-                                                 ctypes.c_void_p(info.data_ptr()), _lib.ENGINES[engine])
+    if triangles is None:
+        wins = (eq_name == "cholesky" and out_zeroed and n >= 48) or (eq_name == "lyapunov" and n >= 64)
+        triangles = wins and n % 2 == 0 and all(a.is_pinned() for a in arrs) and out.is_pinned()
+    flags = (_lib.HOST_TRIANGLES if triangles else 0) | (_lib.HOST_X_ZEROED if out_zeroed else 0)
+    rc = _lib.lib.lagen_b200_execute_host_flags(EQ_CODES[eq_name], ctypes.addressof(arr), len(stmts), n, b,
+                                                batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
+                                                ctypes.c_void_p(info.data_ptr()), _lib.ENGINES[engine], flags)
     _lib.check(rc, f"{eq_name} host n={n} b={b}")
     return out, info
 

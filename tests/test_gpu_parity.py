@@ -442,3 +442,52 @@ def test_padded_sizes_with_minus_one_diagonal(eq, oracle_mod):
                 assert info.cpu().tolist() == [0, 0, 0, 0], (eq, n, v, b)
                 ref, _ = oracle_mod.execute(eq, builtin_variants(eq)[v].statements, n, b, ins_h)
                 assert rel_diff(X.cpu().numpy(), ref).max() <= REL_TOL
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+def test_unread_triangles_are_ignored(eq):
+    """The structurally unused triangles (A's and S's strict lower, L's strict
+    upper, U's strict lower — never read by the reference either,
+    test_acceptance.py:167-184) may hold anything: NaN there changes nothing,
+    on every engine x variant x b.  This is what lets the host path move
+    triangles only."""
+    for n in (16, 64):
+        ins = executor.generate(eq, n, seed=9, batch=8)
+        dirty = [t.clone() for t in ins]
+        lower = torch.tril(torch.ones(n, n, dtype=torch.bool, device="cuda"), -1)
+        if eq == "cholesky":
+            dirty[0][:, lower] = float("nan")
+        elif eq == "lyapunov":
+            dirty[0][:, lower.T] = float("nan")
+            dirty[1][:, lower] = float("nan")
+        else:
+            dirty[0][:, lower.T] = float("nan")
+            dirty[1][:, lower] = float("nan")
+        for v, b, engine in engine_runs(eq, n, [v.index for v in builtin_variants(eq)]):
+            X0, _ = executor.solve(eq, ins, variant=v, b=b, engine=engine)
+            X1, info = executor.solve(eq, dirty, variant=v, b=b, engine=engine, check=False)
+            assert int(info.abs().sum()) == 0, (eq, n, v, b, engine)
+            assert torch.equal(X0, X1), (eq, n, v, b, engine)
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
+def test_host_triangles_equal_device_path(eq):
+    """solve_host moving triangles only (zero-copy from pinned memory), with
+    and without the caller-zeroed X of the reference contract, equals the
+    device path bit for bit; unpinned buffers and odd n take the dense path."""
+    from paper_1906_08613_b200 import _lib
+    for n in (16, 62, 128):
+        batch = 3000 if n < 100 else 700
+        ins = executor.generate(eq, n, seed=4, batch=batch)
+        Xd, _ = executor.solve(eq, ins)
+        host = [t.cpu().pin_memory() for t in ins]
+        for zeroed in ((False, True) if eq == "cholesky" else (False,)):
+            out = torch.zeros((batch, n, n), dtype=torch.float64).pin_memory() if zeroed else \
+                torch.full((batch, n, n), float("nan"), dtype=torch.float64).pin_memory()
+            Xh, info = executor.solve_host(eq, host, out=out, triangles=True, out_zeroed=zeroed)
+            assert int(info.abs().sum()) == 0
+            assert torch.equal(Xh, Xd.cpu()), (eq, n, zeroed)
+        h2d, d2h = _lib.host_bytes(EQ_CODES[eq], n, batch, _lib.HOST_TRIANGLES)
+        assert h2d < len(ins) * batch * n * n * 8
+    with pytest.raises(errors.LagenError):
+        executor.solve_host(eq, [t.cpu() for t in executor.generate(eq, 16, seed=4, batch=4)], triangles=True)
