@@ -15,8 +15,9 @@ from pathlib import Path
 REPO = Path(__file__).resolve().parents[1]
 OUT = REPO / "gpurun_out"
 PROF = REPO / "profiles"
-FULL = [("chol128_rows_v1b8", "full_chol128"), ("chol92_rowspad_v1", "full_chol92"),
-        ("sylv128_wave_v13", "full_sylv128"), ("lyap64_wave_v5", "full_lyap64")]
+FULL_ALL = [("chol128_rows_v1b8", "full_chol128"), ("chol92_rowspad_v1", "full_chol92"),
+        ("sylv128_pipe_v13", "full_sylv128"), ("lyap64_pipe_v5", "full_lyap64"),
+        ("sylv64_pipe_v13", "full_sylv64"), ("lyap128_pipe_v5", "full_lyap128")]
 METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "gpu__time_duration.sum",
            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__block_size", "launch__grid_size",
@@ -60,6 +61,11 @@ def main():
     line = (OUT / "bench_final.log").read_text().strip().splitlines()[-1]
     bench = json.loads(line)
     (PROF / f"{tag}_bench.json").write_text(json.dumps(bench) + "\n")
+    if (OUT / "bench_detail.json").exists():
+        shutil.copy(OUT / "bench_detail.json", PROF / f"{tag}_bench_detail.json")
+    for extra, dst in (("bench_reference.log", f"{tag}_bench_reference_arm.json"), ("pytest_gpu.log", f"{tag}_pytest_gpu.log")):
+        if (OUT / extra).exists():
+            shutil.copy(OUT / extra, PROF / dst)
     md = []
     for name in ("chol-sweep", "lyap-sweep", "sylv-sweep"):
         ls = launches(name, 32)
@@ -76,6 +82,7 @@ def main():
         md.append("")
     (PROF / f"{tag}_ncu_launches_sweeps.md").write_text("\n".join(md))
     shutil.copy(OUT / "launches_chol-sweep.csv", PROF / f"{tag}_ncu_launches_chol_sweep.csv")
+    FULL = [(l, r) for l, r in FULL_ALL if (OUT / f"{r}.ncu-rep").exists()]
     cols = {}
     for label, rep in FULL:
         out = subprocess.run(["ncu", "-i", str(OUT / f"{rep}.ncu-rep"), "--page", "raw", "--csv", "--metrics",

@@ -4,7 +4,7 @@
 # kernels.  Each ncu command runs only after the same command exited 0.
 set -u
 O=gpurun_out
-python bench.py --steps 10 --warmup 3 > $O/bench_final.log 2>&1; echo "bench rc=$?"
+python bench.py --steps 10 --warmup 3 --json-out $O/bench_detail.json > $O/bench_final.log 2>&1; echo "bench rc=$?"
 for w in chol-sweep lyap-sweep sylv-sweep; do
   CMD="python bench.py --workload $w --steps 1 --warmup 1 --no-cpu --no-e2e --no-extra"
   $CMD > $O/plain_$w.log 2>&1 && \
@@ -19,5 +19,7 @@ run1() {  # name, run_one args
 }
 KRE=chol_rows_kernel run1 chol128 --eq cholesky --n 128 --variant 1 --b 8 --engine rows
 KRE=chol_rows_kernel run1 chol92 --eq cholesky --n 92 --variant 1 --b 4 --engine rowspad
-KRE=wave_kernel run1 sylv128 --eq sylvester --n 128 --variant 13 --b 8 --engine wave
-KRE=wave_kernel run1 lyap64 --eq lyapunov --n 64 --variant 5 --b 8 --engine wave
+KRE=pipe_kernel run1 sylv128 --eq sylvester --n 128 --variant 13 --b 8 --engine pipe
+KRE=pipe_kernel run1 lyap64 --eq lyapunov --n 64 --variant 5 --b 8 --engine pipe
+KRE=pipe_kernel run1 sylv64 --eq sylvester --n 64 --variant 13 --b 8 --engine pipe
+KRE=pipe_kernel run1 lyap128 --eq lyapunov --n 128 --variant 5 --b 8 --engine pipe
