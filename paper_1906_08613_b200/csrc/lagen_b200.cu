@@ -16,10 +16,8 @@
 #include "lagen_b200.h"
 #include "registry.cuh"
 #include "registry_col.cuh"
-#include "registry_df.cuh"
 #include "registry_rows.cuh"
 #include "registry_warp.cuh"
-#include "registry_wave.cuh"
 #include "registry_pipe.cuh"
 #include "registry_rowsweep.cuh"
 #include "variants_table.h"
@@ -67,16 +65,6 @@ const ColEntry* find_col(int eq, int n, int b, int variant) {
   return nullptr;
 }
 
-const DfEntry* find_df(int eq, int n, int b, int variant) {
-  if (eq < 0 || eq > 2 || variant < 0) return nullptr;
-  for (int p = 0; p < kDfParts; ++p) {
-    const DfTable& t = kDfTables[p];
-    for (int i = 0; i < *t.n; ++i)
-      if (t.e[i].eq == eq && t.e[i].n == n && t.e[i].b == b && t.e[i].variant == variant) return &t.e[i];
-  }
-  return nullptr;
-}
-
 const RowsEntry* find_rows(int eq, int n, int b, int variant) {
   if (eq != 0 || variant < 0) return nullptr;
   for (int p = 0; p < kRowsParts; ++p) {
@@ -95,19 +83,6 @@ const RowsEntry* find_rows_pad(int eq, int n, int b, int variant) {
     const RowsPadTable& t = kRowsPadTables[p];
     for (int i = 0; i < *t.n; ++i)
       if (t.e[i].n == n) return &t.e[i];
-  }
-  return nullptr;
-}
-
-// wave engine: Lyapunov v5 / Sylvester v13 (the right-looking variants whose
-// tile-level order it follows, wave.cuh), any block size the variant runs at
-const WaveEntry* find_wave(int eq, int n, int b, int variant) {
-  (void)b;
-  if (!((eq == 1 && variant == 5) || (eq == 2 && variant == 13))) return nullptr;
-  for (int p = 0; p < kWaveParts; ++p) {
-    const WaveTable& t = kWaveTables[p];
-    for (int i = 0; i < *t.n; ++i)
-      if (t.e[i].eq == eq && t.e[i].n == n) return &t.e[i];
   }
   return nullptr;
 }
@@ -366,9 +341,9 @@ int lagen_b200_engine_supported(int eq, int n, int b, int variant, int engine) {
     case LAGEN_ENGINE_GENERIC: return find_entry(eq, n, b) ? 1 : 0;
     case LAGEN_ENGINE_WARP: return find_warp(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_COLUMN: return find_col(eq, n, b, variant) ? 1 : 0;
-    case LAGEN_ENGINE_DATAFLOW: return find_df(eq, n, b, variant) ? 1 : 0;
+    case LAGEN_ENGINE_DATAFLOW: return 0;  // removed (never selected by the measured dispatch table)
     case LAGEN_ENGINE_ROWS: return find_rows(eq, n, b, variant) ? 1 : 0;
-    case LAGEN_ENGINE_WAVE: return find_wave(eq, n, b, variant) ? 1 : 0;
+    case LAGEN_ENGINE_WAVE: return 0;  // superseded by the pipe engine
     case LAGEN_ENGINE_ROWS_PAD: return find_rows_pad(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_PIPE: return find_pipe(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_ROWSWEEP: return find_rowsweep(eq, n, b, variant) ? 1 : 0;
@@ -456,40 +431,32 @@ int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int 
       return fail(LAGEN_EUNSUPPORTED, "no column-engine instance for this (variant, n, b)");
     if (engine == LAGEN_ENGINE_WARP && !w)
       return fail(LAGEN_EUNSUPPORTED, "no warp-engine instance for this (variant, n, b)");
-    const DfEntry* d = (engine == LAGEN_ENGINE_DATAFLOW) ? find_df(eq, n, b, v) : nullptr;
-    if (engine == LAGEN_ENGINE_DATAFLOW && !d)
-      return fail(LAGEN_EUNSUPPORTED, "no dataflow-engine instance for this (variant, n, b)");
+    if (engine == LAGEN_ENGINE_DATAFLOW || engine == LAGEN_ENGINE_WAVE)
+      return fail(LAGEN_EUNSUPPORTED, "the dataflow and wave engines were removed (never the fastest measured path)");
     // AUTO: the rows engine (Cholesky v1, n > 32) is the fastest measured path
     // (dispatch_table.json); the register column engine below that
     const RowsEntry* st =
         (engine == LAGEN_ENGINE_ROWS || (engine == LAGEN_ENGINE_AUTO && n > 32)) ? find_rows(eq, n, b, v) : nullptr;
     if (engine == LAGEN_ENGINE_ROWS && !st)
       return fail(LAGEN_EUNSUPPORTED, "no rows-engine instance for this (variant, n, b)");
-    // AUTO: the wave engine for the right-looking Lyapunov / Sylvester
-    // variants at n >= 16 (dispatch_table.json measures the rest)
     // AUTO: the pipe engine for the right-looking Lyapunov / Sylvester
     // variants (dispatch_table.json measures the rest)
     const PipeEntry* pp =
         (engine == LAGEN_ENGINE_PIPE || engine == LAGEN_ENGINE_AUTO) ? find_pipe(eq, n, b, v) : nullptr;
     if (engine == LAGEN_ENGINE_PIPE && !pp)
       return fail(LAGEN_EUNSUPPORTED, "no pipe-engine instance for this (variant, n, b)");
-    const WaveEntry* wv = (engine == LAGEN_ENGINE_WAVE) ? find_wave(eq, n, b, v) : nullptr;
     // AUTO: the rowsweep engine whenever b = n (n <= 32)
     const RowSweepEntry* rs =
         (engine == LAGEN_ENGINE_ROWSWEEP || engine == LAGEN_ENGINE_AUTO) ? find_rowsweep(eq, n, b, v) : nullptr;
     if (engine == LAGEN_ENGINE_ROWSWEEP && !rs)
       return fail(LAGEN_EUNSUPPORTED, "no rowsweep-engine instance for this (variant, n, b): it runs b = n, n <= 32");
-    if (engine == LAGEN_ENGINE_WAVE && !wv)
-      return fail(LAGEN_EUNSUPPORTED, "no wave-engine instance for this (variant, n, b)");
     const RowsEntry* rp = (engine == LAGEN_ENGINE_ROWS_PAD) ? find_rows_pad(eq, n, b, v) : nullptr;
     if (engine == LAGEN_ENGINE_ROWS_PAD && !rp)
       return fail(LAGEN_EUNSUPPORTED, "no padded rows-engine instance for this (variant, n, b)");
     if (rp) fn = rp->launch;
     else if (rs) fn = rs->launch;
     else if (pp) fn = pp->launch;
-    else if (wv) fn = wv->launch;
     else if (st) fn = st->launch;
-    else if (d) fn = d->launch;
     else if (c) fn = c->launch;
     else if (w) fn = w->launch;
   }

@@ -98,12 +98,19 @@ struct PCfg {
   static constexpr int THREADS = PP * GW * 32;
   static constexpr size_t SMEM = (size_t)PP * SLOT * 8;
   static constexpr int mn(int a, int b) { return a < b ? a : b; }
-  // CTAs per SM for __launch_bounds__: what shared memory and threads allow,
-  // as long as that leaves >= RMIN registers per thread (split roles: the
-  // solve's live state; solo: solve + accumulators)
+  // CTAs per SM for __launch_bounds__ (it sets the register budget).  Split
+  // roles: measured per tile count over MINB = 1..8 at the BASELINE batches
+  // (tools/experiments/pipe_bench.cu, profiles/r02_pipe_minb_sweep.txt) — more
+  // CTAs hide the solve's latency until the accumulators spill (Lyapunov holds
+  // T + 1 tiles per updater warp: 96 registers spill from T = 9 on).  Solo
+  // mode: what shared memory and threads allow with >= 128 registers.
   static constexpr int RMIN = MODE == 1 ? 128 : 96;
   static constexpr int fitb(int b) { return (b <= 1 || 65536 / (THREADS * b) >= RMIN) ? b : fitb(b - 1); }
-  static constexpr int MINB0 = fitb(mn(smem_fit(PP), 2048 / THREADS));
+  static constexpr int MINB_FIT = fitb(mn(smem_fit(PP), 2048 / THREADS));
+  static constexpr int kLyapMinb[17] = {1, 1, 1, 1, 7, 7, 6, 4, 4, 4, 2, 2, 2, 2, 2, 1, 1};
+  static constexpr int kSylvMinb[17] = {1, 1, 1, 1, 4, 4, 4, 3, 2, 2, 2, 1, 1, 1, 1, 1, 1};
+  static constexpr int MINB_TAB = mn(EQ == 1 ? kLyapMinb[T] : kSylvMinb[T], mn(smem_fit(PP), 2048 / THREADS));
+  static constexpr int MINB0 = (MODE == 1 || T < 4) ? MINB_FIT : MINB_TAB;
 #ifdef LAGEN_PIPE_MINB
   static constexpr int MINB = LAGEN_PIPE_MINB;
 #else
@@ -155,7 +162,7 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
   const int w = MODE == 1 ? 0 : wi;                          // updater index
   const int sv = MODE == 1 ? 0 : (wi >= NU ? wi - NU : 0);  // solver index
   const int srank = MODE == 1 ? lane : rank - NU * 32;
-  double* scr = Zt + 64 + sv * 256 + lane * 8;
+  double* scr = Zt + 64 + sv * 256 + lane;  // pivot reciprocals: row r of the tile at scr[32 r] (conflict-free)
   const int g = lane >> 2, t = lane & 3;
   const int oA0 = sw(g, t), oA1 = sw(g, t + 4), oB0 = sw(t, g), oB1 = sw(t + 4, g);
   const int oR = (7 + g) * 10 + 2 * t;  // C fragment in a solve scratch (row-major, pitch 10, 7 pad rows)
@@ -405,24 +412,25 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
     const double* Ld = Lt + ltidx(I, I) * 64;
     const double* Ud = EQ == 2 ? Ut + utidx(J, J) * 64 : Lt + ltidx(J, J) * 64;
     auto uat = [&](int k) -> double { return EQ == 2 ? Ud[sw(k, c)] : Ud[sw(c, k)]; };
+    // uo[j] = U_JJ(j, c) for j <= c - 2 (older row values, from the scratch),
+    // u1 = U_JJ(c - 1, c) (newest, by shuffle); 0 elsewhere
+    double uo[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    double u1 = 0.0;
     {
       const double ucc = uat(c);
       double dg[8];
 #pragma unroll
       for (int r = 0; r < 8; ++r) dg[r] = Ld[sw(r, r)];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) scr[r] = (8 * I + r < N && 8 * J + c < N) ? recip(dg[r] + ucc) : 0.0;
-    }
-    // uo[j] = U_JJ(j, c) for j <= c - 2 (older row values, from the scratch),
-    // u1 = U_JJ(c - 1, c) (newest, by shuffle); 0 elsewhere
-    double uo[7];
+      for (int r = 0; r < 8; ++r) scr[32 * r] = (8 * I + r < N && 8 * J + c < N) ? recip(dg[r] + ucc) : 0.0;
 #pragma unroll
-    for (int j = 0; j < 7; ++j) {
-      const double v = uat(j);
-      uo[j] = j + 2 <= c ? v : 0.0;
+      for (int j = 0; j < 6; ++j) {
+        const double v = uat(j);
+        uo[j] = j + 2 <= c ? v : 0.0;
+      }
+      const double u1v = uat(c >= 1 ? c - 1 : 0);
+      u1 = c >= 1 ? u1v : 0.0;
     }
-    const double u1v = uat(c >= 1 ? c - 1 : 0);
-    const double u1 = c >= 1 ? u1v : 0.0;
     if constexpr (MODE == 0) asm volatile("bar.sync 2, %0;" ::"n"(P::THREADS) : "memory");
     else __syncwarp();
     if (sv == 0) stamp(4 * (d + 1) + 1);
@@ -432,9 +440,14 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
     // shuffle and the older ones from the scratch row (written >= 2 steps ago)
     double* Sl = Sq + (7 - c) * 10 + c;             // + 10 s: element (s - c, c)
     const double* Sr = Sq + (7 - c) * 10;           // + 10 s: row s - c
-    const double* pl = scr - c;                     // + s: pivot of row s - c
+    // pivot of row s - c: scr[32 ((s - c) & 7)] (rows outside the tile wrap around; their x is masked)
+    const int pl0 = (8 - c) & 7;
+    auto pl = [&](int s) -> double { return scr[32 * ((pl0 + s) & 7)]; };
     const double* Ll = Lsh + (7 + 8 * I - c) * 10;  // + 10 s: L_II column s - c
     const int src1 = (lane & ~7) | (c >= 1 ? c - 1 : c);
+    // (letting the groups without a tile skip the solve — no instructions, no
+    // wavefronts — measured 5-17 % slower: the divergence costs more registers)
+    const unsigned lm = 0xffffffffu;
     double y[8];
 #pragma unroll
     for (int s = 0; s < 8; ++s) y[s] = Sl[10 * s];
@@ -443,14 +456,13 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
     // step s, so visible after the previous step's __syncwarp)
     auto rowsum = [&](int s) -> double {
       const double2* rw = reinterpret_cast<const double2*>(Sr + 10 * s);
-      const double2 r0 = rw[0], r1 = rw[1], r2 = rw[2], r3 = rw[3];
+      const double2 r0 = rw[0], r1 = rw[1], r2 = rw[2];  // (columns 6, 7 are never "older": j <= c - 2 <= 5)
       double t0 = r0.x * uo[0];
       double t1 = r0.y * uo[1];
       t0 = fma(r1.x, uo[2], t0);
       t1 = fma(r1.y, uo[3], t1);
       t0 = fma(r2.x, uo[4], t0);
       t1 = fma(r2.y, uo[5], t1);
-      t0 = fma(r3.x, uo[6], t0);
       return t0 + t1;
     };
     // Program order matters (in-order issue): each step first loads what the
@@ -458,7 +470,7 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
     // -> MUL -> x, shuffles x on right away, and only then the pushes and
     // the next row sum (whose loads have landed by then)
     double x1 = 0.0;                       // x(r, c-1) of the current step, by shuffle
-    double pcur = pl[0];
+    double pcur = pl(0);
     double vpre = y[0] - rowsum(0);        // y - older row contributions of the current step
     auto step = [&](int s, int u) {
       const bool act = (unsigned)(s - c) < 8u;
@@ -466,17 +478,17 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
       const double2* lc = reinterpret_cast<const double2*>(Ll + 10 * s);
       const double2 la = lc[0], lb = lc[1], lcc = lc[2], ld = lc[3];
       const double2* rw = reinterpret_cast<const double2*>(Sr + 10 * (s + 1));
-      double2 r0, r1, r2, r3;
+      double2 r0, r1, r2;
       double pnxt = 0.0, yref = 0.0;
       if (s < 14) {
-        r0 = rw[0], r1 = rw[1], r2 = rw[2], r3 = rw[3];
-        pnxt = pl[s + 1];
+        r0 = rw[0], r1 = rw[1], r2 = rw[2];
+        pnxt = pl(s + 1);
       }
       if (s + 8 <= 14) yref = Sl[10 * (s + 8)];
       // the chain
       const double v = fma(-x1, u1, vpre);
       const double x = act ? v * pcur : 0.0;
-      x1 = __shfl_sync(0xffffffffu, x, src1);
+      x1 = __shfl_sync(lm, x, src1);
       // push into the next row first (the next step's vpre), then the rest
       y[(u + 1) & 7] = fma(-la.y, x, y[(u + 1) & 7]);
       if (s < 14) {
@@ -486,7 +498,6 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
         t1 = fma(r1.y, uo[3], t1);
         t0 = fma(r2.x, uo[4], t0);
         t1 = fma(r2.y, uo[5], t1);
-        t0 = fma(r3.x, uo[6], t0);
         vpre = y[(u + 1) & 7] - (t0 + t1);
         pcur = pnxt;
       }
@@ -495,7 +506,7 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
 #pragma unroll
       for (int e = 2; e < 8; ++e) y[(u + e) & 7] = fma(-coef[e], x, y[(u + e) & 7]);
       if (s + 8 <= 14) y[u] = yref;
-      __syncwarp();
+      __syncwarp(lm);
     };
 #pragma unroll
     for (int u = 0; u < 8; ++u) step(u, u);
