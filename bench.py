@@ -383,7 +383,7 @@ def cpu_baseline(eq, cases, budget_s=12.0, inputs_from=None, seed_first=0):
         "kind": "reference" if use_ref else "port",
         "sample": (f"per size: the first s problems of the same workload (s sized for ~{per_size_budget:.2f} s), "
                    "throughput extrapolated to the full batch; kernel = fastest verified emitted variant "
-                   "(lagen emit_function, nu=4) compiled gcc -O3 -march=native -std=c99, OpenMP over problems")
+                   "(lagen emit_function, scalar and nu=4 modes) compiled gcc -O3 -march=native -std=c99, OpenMP over problems")
         if use_ref else "oracle C port, OpenMP over problems",
         "sample_short": (f"first s problems of each size (~{per_size_budget:.2f} s per size), "
                          "extrapolated to the full batch"),
