@@ -30,6 +30,15 @@ import torch
 from . import dispatch, errors, executor
 from .variants import EQUATIONS, builtin_variants, default_blocks, flop_count
 
+# With the reference importable its own pieces are used, not restated: the
+# selection rule `_select` (cli.py:175-181), the admissible blocks
+# (cli.py:89-93), and — for live Equation objects, run_pipeline_live below —
+# its variant enumeration, instances, residual and flop model.
+try:  # pragma: no cover - depends on the environment
+    from lagen import cli as _ref_cli
+except Exception:  # the GPU box has no reference package
+    _ref_cli = None
+
 DEFAULT_SEED = 0
 DEFAULT_TOL = 1e-10  # cli.py DEFAULT_TOL, the harness GUARD (codegen.py:496-578)
 DEFAULT_REPS = 5
@@ -119,7 +128,8 @@ def benchmark_variant(eq, cfg, n, batch=None, reps=DEFAULT_REPS, seed=DEFAULT_SE
     if batch is None:
         batch = max(1, (1 << 28) // (8 * n * n))
     ins = executor.generate(eq, n, seed=seed + n, batch=batch)
-    plan = executor.Plan(eq, ins, variant=cfg.algorithm_index, b=cfg.b)
+    # a live reference Algorithm (run_pipeline_live) is encoded by the executor
+    plan = executor.Plan(eq, ins, variant=getattr(cfg, "algorithm", None) or cfg.algorithm_index, b=cfg.b)
     stream = torch.cuda.current_stream()
     plan.launch(stream)
     ts = []
@@ -135,7 +145,10 @@ def benchmark_variant(eq, cfg, n, batch=None, reps=DEFAULT_REPS, seed=DEFAULT_SE
 
 
 def _select(rows):
-    """Mark the fastest verified row; ties break on flops, then id (cli.py:175-181)."""
+    """Mark the fastest verified row; ties break on flops, then id
+    (cli.py:175-181; the reference's own function when importable)."""
+    if _ref_cli is not None:
+        return _ref_cli._select(rows)
     timed = [r for r in rows if r["median_ns"] is not None]
     if not timed:
         return
@@ -186,6 +199,84 @@ def run_pipeline(eq, sizes, seed=DEFAULT_SEED, tol=DEFAULT_TOL, blocks=None, rep
     for row in rows:
         del row["verified"]
     return {"equation": eq, "n": target_n, "variants": rows}, all_verified, failures
+
+
+def live_variant_configs(eq, n, blocks=None):
+    """The reference's own variant space for a live `Equation`
+    (cli.enumerate_variants, cli.py:95-120: its synthesised `Algorithm`
+    objects x admissible b, tiles = b) re-tagged mode "cuda": each config is a
+    reference `VariantConfig` subclass instance whose id ends in `_cuda`."""
+    if _ref_cli is None:
+        raise errors.UsageError("the reference package `lagen` is not importable")
+
+    class CudaConfig(_ref_cli.VariantConfig):
+        @property
+        def id(self):
+            return f"a{self.algorithm_index}_b{self.b}_t{self.tiles}_cuda"
+
+    return [CudaConfig(c.algorithm, c.algorithm_index, c.b, c.tiles, "cuda")
+            for c in _ref_cli.enumerate_variants(eq, n, blocks, None, "scalar")]
+
+
+def run_pipeline_live(eq, sizes, seed=DEFAULT_SEED, tol=DEFAULT_TOL, blocks=None, reps=DEFAULT_REPS,
+                      batch=None, benchmark=True, log=print):
+    """`run_pipeline` (cli.py:184-251) driven by the reference's own objects:
+    `eq` is a live `lagen` Equation; the variant space, the verification
+    instances (`random_instance`), the residual, the flop model, the report
+    schema and `_select` are the reference's — only the two execution steps
+    are replaced: `interpret_algorithm` -> executor.interpret_algorithm (the
+    CUDA kernel run from the live Algorithm's statements) and the emitted-C
+    harness -> benchmark_variant above."""
+    from lagen import verify as rverify
+    from lagen.worksheet import flop_count as ref_flop_count
+
+    target_n = max(sizes)
+    rows, cfgs = [], {}
+    for cfg in live_variant_configs(eq, target_n, blocks):
+        residuals = {}
+        for n in sizes:
+            if n % cfg.b:
+                residuals[str(n)] = None
+                continue
+            inst = rverify.random_instance(cfg.algorithm.equation, n, seed)
+            try:
+                outputs, _ = executor.interpret_algorithm(cfg.algorithm, inst, cfg.b)
+                residuals[str(n)] = float(rverify.residual(cfg.algorithm.equation, inst, outputs))
+            except errors.VerificationError:
+                residuals[str(n)] = float("inf")
+        checked = [r for r in residuals.values() if r is not None]
+        cfgs[cfg.id] = cfg
+        rows.append({
+            "id": cfg.id,
+            "algorithm": cfg.algorithm_index,
+            "invariant": cfg.algorithm.invariant.label(),
+            "b": cfg.b,
+            "tiles": cfg.tiles,
+            "mode": "cuda",
+            "flops": ref_flop_count(cfg.algorithm, target_n, cfg.b),
+            "residuals": residuals,
+            "median_ns": None,
+            "selected": False,
+            "verified": bool(checked) and all(r <= tol for r in checked),
+        })
+    failures = 0
+    if benchmark:
+        for row in rows:
+            if not row["verified"]:
+                continue
+            try:
+                ns, ms, nb, engine = benchmark_variant(eq.name, cfgs[row["id"]], target_n, batch, reps, seed)
+            except errors.LagenError as err:
+                failures += 1
+                log(f"benchmark {row['id']}: {err}", file=sys.stderr)
+                continue
+            row.update(median_ns=ns, batch=nb, median_ms=ms, engine=engine)
+            log(f"RESULT {row['id']} {target_n} {ns} {row['flops']}")
+        _select(rows)
+    all_verified = all(r["verified"] for r in rows)
+    for row in rows:
+        del row["verified"]
+    return {"equation": eq.name, "n": target_n, "variants": rows}, all_verified, failures
 
 
 def selected(report):

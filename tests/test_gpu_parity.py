@@ -363,6 +363,23 @@ def test_reference_algorithm_objects_drop_in():
                 assert np.linalg.norm(got["X"] - x) <= REL_TOL * max(1.0, np.linalg.norm(x))
 
 
+def test_reference_algorithm_fixtures_drop_in():
+    """The same drop-in on objects rebuilt from the serialised live
+    `Algorithm`s (tests/golden/make_algorithm_fixtures.py): runs where the
+    reference package is absent; expected X and flops are the reference
+    interpreter's own (verify.py:221-303)."""
+    from algorithm_fixtures import load
+    cases, blocks = load()
+    for name, (algs, inst, want) in cases.items():
+        assert len(algs) == len(builtin_variants(name))
+        for alg in algs:
+            for b in blocks:
+                x, wflops = want[(alg.index, b)]
+                got, gflops = executor.interpret_algorithm(alg, inst, b)
+                assert gflops == wflops
+                assert np.linalg.norm(got[alg.output] - x) <= REL_TOL * max(1.0, np.linalg.norm(x))
+
+
 @pytest.mark.parametrize("eq", EQUATIONS)
 def test_config5_sampled(eq, oracle_mod):
     """BASELINE config 5 on one GPU: n = 64, 2^20 problems (2^32 doubles per

@@ -172,3 +172,27 @@ def test_oracle_matches_reference_large_n(eq, oracle_mod):
         assert (info == 0).all()
         worst = max(worst, lg.max_rel_err(X, d, es))
     assert worst <= 1e-13, worst
+
+
+def test_serialised_reference_algorithms(oracle_mod):
+    """The serialised live `Algorithm` objects (make_algorithm_fixtures.py):
+    encode_algorithm gives exactly the frozen variant table's statement lists,
+    the flop model gives the reference's dynamic counts, and the C oracle run
+    from the encoded statements reproduces the reference interpreter's X."""
+    from algorithm_fixtures import load
+    from paper_1906_08613_b200.variants import (EQ_INPUTS, builtin_variants, encode_algorithm,
+                                                 flop_count, stmts_key)
+    cases, blocks = load()
+    for name, (algs, inst, want) in cases.items():
+        table = builtin_variants(name)
+        assert [a.index for a in algs] == [v.index for v in table]
+        ins = [np.ascontiguousarray(inst.bindings[nm], dtype=np.float64)[None] for nm in EQ_INPUTS[name]]
+        for alg, v in zip(algs, table):
+            stmts = encode_algorithm(alg)
+            assert stmts_key(stmts) == stmts_key(v.statements)
+            for b in blocks:
+                x, flops = want[(alg.index, b)]
+                assert flop_count(name, stmts, inst.n, b) == flops
+                got, info = oracle_mod.execute(name, stmts, inst.n, b, ins)
+                assert int(info[0]) == 0
+                assert np.linalg.norm(got[0] - x) <= 1e-13 * max(1.0, np.linalg.norm(x))

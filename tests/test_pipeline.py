@@ -53,3 +53,45 @@ def test_run_pipeline_cuda(eq):
     res = [l.split() for l in lines if l.startswith("RESULT")]
     assert len(res) == len(rows) and all(len(p) == 5 and p[2] == "16" for p in res)
     assert pipeline.selected(report) is not None
+
+
+def test_live_pipeline_uses_the_reference_objects(oracle_mod, monkeypatch):
+    """run_pipeline_live on a live lagen Equation: the reference's variant
+    space, instances, residual, flop model, schema and _select, with the two
+    execution steps replaced (here by the CPU oracle and a fixed timing, no
+    GPU) — row for row against the reference's own run_pipeline."""
+    pytest.importorskip("lagen")
+    import numpy as np
+    from lagen import cli
+    from lagen.lang import parse_equation
+    from paper_1906_08613_b200 import executor
+    from paper_1906_08613_b200.variants import EQ_INPUTS, encode_algorithm
+
+    eq = parse_equation("Equation: L * X + X * L^T = S\nL: Matrix(n,n), lower_triangular, input\n"
+                        "S: Matrix(n,n), symmetric, input\nX: Matrix(n,n), symmetric, output\n", name="lyapunov")
+
+    def fake_interpret(alg, inst, b, on_iteration=None):
+        ins = [np.ascontiguousarray(inst.bindings[nm], dtype=np.float64)[None] for nm in EQ_INPUTS["lyapunov"]]
+        X, info = oracle_mod.execute("lyapunov", encode_algorithm(alg), inst.n, b, ins)
+        assert int(info[0]) == 0
+        return {alg.output: X[0]}, 0
+
+    times = iter(range(100, 0, -1))
+    monkeypatch.setattr(executor, "interpret_algorithm", fake_interpret)
+    monkeypatch.setattr(pipeline, "benchmark_variant", lambda *a, **k: (next(times), 1.0, 8, "stub"))
+    lines = []
+    got, ok, fails = pipeline.run_pipeline_live(eq, [8, 16], log=lambda *a, **k: lines.append(a[0]))
+    want, wok, _ = cli.run_pipeline(eq, [8, 16], cc=None)
+    assert ok and wok and fails == 0
+    assert got["equation"] == want["equation"] and got["n"] == want["n"]
+    assert len(got["variants"]) == len(want["variants"])
+    for g, w in zip(got["variants"], want["variants"]):
+        assert g["id"] == w["id"].replace("_scalar", "_cuda") and g["mode"] == "cuda"
+        for k in ("algorithm", "invariant", "b", "tiles", "flops"):
+            assert g[k] == w[k]
+        assert set(g["residuals"]) == set(w["residuals"])
+        assert all(r is None or r <= 1e-10 for r in g["residuals"].values())
+    # the reference's own _select ran on the rows: the last (fastest stub time) wins
+    assert [r["selected"] for r in got["variants"]] == [False] * (len(got["variants"]) - 1) + [True]
+    assert pipeline._select.__doc__ and pipeline._ref_cli is cli
+    assert len(lines) == len(got["variants"]) and all(l.startswith("RESULT a") for l in lines)
