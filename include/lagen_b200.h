@@ -146,6 +146,10 @@ int lagen_b200_execute(int eq, const lagen_stmt* stmts, int nstmts, int n, int b
  * matrix, kernels.py:100-130): one lane per row, column-by-column forward
  * substitution with the X U part lane-local (rowsweep.cuh); any variant */
 #define LAGEN_ENGINE_ROWSWEEP 9
+/* Cholesky v1, n = 4 mod 8 (requested as b = 4): the rows engine's b = 8
+ * schedule after a first 4 x 4 block row — v1's statements over the
+ * partition 4, 8, 8, ..., 8, unpadded (chol_rows.cuh, F4) */
+#define LAGEN_ENGINE_ROWS_MIX 10
 int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
                               long long batch, const double* const* inputs, double* X,
                               int* info, void* stream, int engine);

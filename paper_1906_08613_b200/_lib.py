@@ -69,7 +69,7 @@ EXPORTED = (
 )
 HOST_TRIANGLES = 1
 HOST_X_ZEROED = 2
-ENGINES = {"auto": 0, "generic": 1, "warp": 2, "column": 3, "dataflow": 4, "rows": 5, "wave": 6, "rowspad": 7, "pipe": 8, "rowsweep": 9}
+ENGINES = {"auto": 0, "generic": 1, "warp": 2, "column": 3, "dataflow": 4, "rows": 5, "wave": 6, "rowspad": 7, "pipe": 8, "rowsweep": 9, "rowsmix": 10}
 
 
 def host_bytes(eq_code, n, batch, flags=0):

@@ -23,6 +23,8 @@
 //   then     block row k streams to HBM (zeros left of the diagonal)
 // Per element the arithmetic is v1's statements (S3 does not depend on S2).
 #pragma once
+#include <type_traits>
+
 #include "engine.cuh"
 
 // Residency (measured over the sweep, profiles/r01_rows_db.txt): single
@@ -397,9 +399,10 @@ __device__ __forceinline__ void trsm(double* xs, int r0, const double* rsb, int 
 
 // block row [r0, r0 + B) -> X (row-major, zeros left of the diagonal)
 template <int N, int B, int NR = N>
-__device__ __forceinline__ void store_rows(double* __restrict__ dst, const double* xs, int r0, int rank, int nthr) {
+__device__ __forceinline__ void store_rows(double* __restrict__ dst, const double* xs, int r0, int rank, int nthr,
+                                           int bsz = B) {
   // warps over the block row's rows, lanes over 16-byte pairs (coalesced)
-  const int nb = r0 + B <= NR ? B : NR - r0;  // real rows of this block row
+  const int nb = r0 + bsz <= NR ? bsz : NR - r0;  // real rows of this block row
   constexpr int H = NR / 2;
   if constexpr (H <= 32 || H % 32 == 0 || H >= LAGEN_ROWS_ROWLOOP_H) {
     const int w = rank >> 5, nw = nthr >> 5, lane = rank & 31;
@@ -455,14 +458,38 @@ inline int pad_mode(int nr) {
   return default_mode(nr + 4, 8);
 }
 
-template <int N, int B, int WG_, int NR = N>
+// mixed-block instances (n = 4 mod 8): {n, WG, mode} measured over
+// WG in {1, 2, 4} x modes {1, 5, 9, 13} at the 256 MiB batches
+// (tools/gpu_rowsmix_tune.sh, profiles/r02_rowsmix_tune.txt)
+constexpr int kRowsMixPick[15][3] = {{12, 1, 5},  {20, 1, 9},   {28, 1, 13},  {36, 1, 9},   {44, 1, 5},
+                                      {52, 1, 1},  {60, 1, 1},   {68, 1, 13},  {76, 2, 13},  {84, 2, 13},
+                                      {92, 2, 13}, {100, 2, 9},  {108, 2, 9},  {116, 4, 1},  {124, 4, 13}};
+inline int mix_wg(int n) {
+  for (const auto& e : kRowsMixPick)
+    if (e[0] == n) return e[1];
+  return pad_wg(n);
+}
+inline int mix_mode(int n) {
+  for (const auto& e : kRowsMixPick)
+    if (e[0] == n) return e[2];
+  return pad_mode(n);
+}
+
+// F4 ("mixed blocks", n = 4 mod 8): the same statements over the partition
+// 4, 8, 8, ..., 8 — a first 4 x 4 block row, then the b = 8 schedule from row
+// 4 on (the loop invariant of v1 holds for any partition sequence, so the
+// result is v1's to rounding).  It replaces running such sizes as the
+// identity-padded n + 4 problem (15-25 % slower than its neighbours: more
+// shared memory per problem and (n + 4)^3 work).
+template <int N, int B, int WG_, int NR = N, bool F4 = false>
 __global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)
     chol_rows_kernel(const double* __restrict__ A, double* __restrict__ X, int* __restrict__ info,
                      long long batch, int mode) {
   const int split_mode = mode & 3, work_split = (mode >> 2) & 3;
   using P = RPolicy<N, WG_>;
   static_assert(P::SLOT == Rows<N>::DOUBLES, "packed rows and upper tiles have the same size");
-  constexpr int WG = P::WG, G = WG * 32, NB = N / B;
+  static_assert(!F4 || (B == 8 && N % 8 == 4 && NR == N && N >= 12), "mixed blocks: n = 4 mod 8 on the b = 8 schedule");
+  constexpr int WG = P::WG, G = WG * 32, NB = F4 ? 1 + (N - 4) / 8 : N / B;
   extern __shared__ double smem[];
   int* gflag = reinterpret_cast<int*>(smem + (size_t)P::P * P::DB * P::SLOT);
   double* rsb_all = reinterpret_cast<double*>(gflag + 32);
@@ -523,20 +550,20 @@ __global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)
 #else
     auto tick = [](int) {};
 #endif
-#pragma unroll 1
-    for (int k = 0; k < NB; ++k) {
-      const int r0 = k * B;
+    // one block row: BB its size (compile time), pB the previous one's
+    auto iter = [&](auto bc, const int r0, const int pB) {
+      constexpr int BB = decltype(bc)::value;
       if constexpr (WG == 1) {
-        if (r0 > 0) s1_tile<N, B>(xs, r0, 0, r0 >> 2);
+        if (r0 > 0) s1_tile<N, BB>(xs, r0, 0, r0 >> 2);
         __syncwarp();
-        leaf<N, B>(xs, r0, gr.rsb, &flag);
-        s3<N, B, WG>(xs, r0, 0, 1, gr, 0, 32, split_mode);
+        leaf<N, BB>(xs, r0, gr.rsb, &flag);
+        s3<N, BB, WG>(xs, r0, 0, 1, gr, 0, 32, split_mode);
         __syncwarp();
-        trsm<N, B>(xs, r0, gr.rsb, gr.rank, G);
+        trsm<N, BB>(xs, r0, gr.rsb, gr.rank, G);
         __syncwarp();
-        store_rows<N, B, NR>(X + off, xs, r0, gr.rank, G);
+        store_rows<N, BB, NR>(X + off, xs, r0, gr.rank, G);
       } else {
-        // level A.  warp 0: the last block row's S1 contribution (K = B; the
+        // level A.  warp 0: the last block row's S1 contribution (K = pB; the
         // rows above were applied one iteration ahead), then the leaf.
         // warps 1..WG-1: store block row k-1, S3 of this block row, and the
         // look-ahead S1 part of block k+1 (all rows above r0 are final).
@@ -547,28 +574,36 @@ __global__ void __launch_bounds__(RPolicy<N, WG_>::WARPS * 32, 1)
         const bool ahead = work_split != 3;
         const bool w0_store = work_split == 1 || work_split == 2, w0_look = work_split == 1;
         if (gr.wig == 0) {
-          if (r0 > 0) s1_tile<N, B>(xs, r0, ahead ? (r0 - B) >> 2 : 0, r0 >> 2);
+          if (r0 > 0) s1_tile<N, BB>(xs, r0, ahead ? (r0 - pB) >> 2 : 0, r0 >> 2);
           __syncwarp();
-          leaf<N, B>(xs, r0, gr.rsb, &flag);
-          if (w0_store && r0 > 0) store_rows<N, B, NR>(X + off, xs, r0 - B, lane, 32);
-          if (ahead && w0_look && r0 + B < N && r0 > 0) s1_tile<N, B>(xs, r0 + B, 0, r0 >> 2);
+          leaf<N, BB>(xs, r0, gr.rsb, &flag);
+          if (w0_store && r0 > 0) store_rows<N, B, NR>(X + off, xs, r0 - pB, lane, 32, pB);
+          if (ahead && w0_look && r0 + BB < N && r0 > 0) s1_tile<N, B>(xs, r0 + BB, 0, r0 >> 2);
         } else {
-          if (!w0_store && r0 > 0) store_rows<N, B, NR>(X + off, xs, r0 - B, gr.rank - 32, 32 * (WG - 1));
+          if (!w0_store && r0 > 0) store_rows<N, B, NR>(X + off, xs, r0 - pB, gr.rank - 32, 32 * (WG - 1), pB);
           if constexpr (WG == 2) {
-            s3<N, B, WG>(xs, r0, 0, 1, gr, 0, 32, split_mode);
+            s3<N, BB, WG>(xs, r0, 0, 1, gr, 0, 32, split_mode);
           } else {
-            s3<N, B, WG>(xs, r0, gr.wig - 1, WG - 1, gr, subbar, 32 * (WG - 1), split_mode);
+            s3<N, BB, WG>(xs, r0, gr.wig - 1, WG - 1, gr, subbar, 32 * (WG - 1), split_mode);
           }
-          if (ahead && !w0_look && r0 + B < N && r0 > 0 && gr.wig == WG - 1) s1_tile<N, B>(xs, r0 + B, 0, r0 >> 2);
+          if (ahead && !w0_look && r0 + BB < N && r0 > 0 && gr.wig == WG - 1) s1_tile<N, B>(xs, r0 + BB, 0, r0 >> 2);
         }
         tick(0);
         gsync<WG>(gr);
         tick(1);
-        trsm<N, B>(xs, r0, gr.rsb, gr.rank, G);
+        trsm<N, BB>(xs, r0, gr.rsb, gr.rank, G);
         tick(2);
         gsync<WG>(gr);
         tick(3);
       }
+    };
+    if constexpr (F4) {
+      iter(std::integral_constant<int, 4>{}, 0, 4);
+#pragma unroll 1
+      for (int k = 1; k < NB; ++k) iter(std::integral_constant<int, 8>{}, 8 * k - 4, k == 1 ? 4 : 8);
+    } else {
+#pragma unroll 1
+      for (int k = 0; k < NB; ++k) iter(std::integral_constant<int, B>{}, k * B, B);
     }
     if constexpr (WG > 1) store_rows<N, B, NR>(X + off, xs, N - B, gr.rank, G);
     if (gr.wig == 0 && lane == 0 && flag) gflag[gr.id] = flag;

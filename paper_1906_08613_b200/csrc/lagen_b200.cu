@@ -87,6 +87,17 @@ const RowsEntry* find_rows_pad(int eq, int n, int b, int variant) {
   return nullptr;
 }
 
+// mixed-block rows engine: Cholesky v1, n = 4 mod 8, partition 4, 8, 8, ...
+const RowsEntry* find_rows_mix(int eq, int n, int b, int variant) {
+  if (eq != 0 || variant != 1 || b != 4) return nullptr;
+  for (int p = 0; p < kRowsMixParts; ++p) {
+    const RowsPadTable& t = kRowsMixTables[p];
+    for (int i = 0; i < *t.n; ++i)
+      if (t.e[i].n == n) return &t.e[i];
+  }
+  return nullptr;
+}
+
 // pipe engine: Lyapunov v5 / Sylvester v13 order at 8x8-tile granularity
 // (pipe.cuh), any block size the variant runs at
 const PipeEntry* find_pipe(int eq, int n, int b, int variant) {
@@ -347,6 +358,7 @@ int lagen_b200_engine_supported(int eq, int n, int b, int variant, int engine) {
     case LAGEN_ENGINE_ROWS_PAD: return find_rows_pad(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_PIPE: return find_pipe(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_ROWSWEEP: return find_rowsweep(eq, n, b, variant) ? 1 : 0;
+    case LAGEN_ENGINE_ROWS_MIX: return find_rows_mix(eq, n, b, variant) ? 1 : 0;
   }
   return 0;
 }
@@ -364,7 +376,7 @@ int lagen_b200_execute_engine(int eq, const lagen_stmt* stmts, int nstmts, int n
 int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                const double* const* inputs, double* X, int* info, void* stream, int engine,
                                unsigned long long* d_prof) {
-  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWSWEEP) return fail(LAGEN_EINVAL, "unknown engine");
+  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWS_MIX) return fail(LAGEN_EINVAL, "unknown engine");
   if (eq < 0 || eq > 2) return fail(LAGEN_EINVAL, "unknown equation");
   if (batch < 0) return fail(LAGEN_EINVAL, "negative batch");
   int rc = validate(eq, stmts, nstmts);
@@ -453,7 +465,11 @@ int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int 
     const RowsEntry* rp = (engine == LAGEN_ENGINE_ROWS_PAD) ? find_rows_pad(eq, n, b, v) : nullptr;
     if (engine == LAGEN_ENGINE_ROWS_PAD && !rp)
       return fail(LAGEN_EUNSUPPORTED, "no padded rows-engine instance for this (variant, n, b)");
-    if (rp) fn = rp->launch;
+    const RowsEntry* rm = (engine == LAGEN_ENGINE_ROWS_MIX) ? find_rows_mix(eq, n, b, v) : nullptr;
+    if (engine == LAGEN_ENGINE_ROWS_MIX && !rm)
+      return fail(LAGEN_EUNSUPPORTED, "no mixed-block rows-engine instance for this (variant, n, b): Cholesky v1, n = 4 mod 8, b = 4");
+    if (rm) fn = rm->launch;
+    else if (rp) fn = rp->launch;
     else if (rs) fn = rs->launch;
     else if (pp) fn = pp->launch;
     else if (st) fn = st->launch;
@@ -654,7 +670,7 @@ int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, 
 int lagen_b200_execute_host_flags(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                   const double* const* h_inputs, double* h_X, int* h_info, int engine, int flags) {
   if (flags & ~(LAGEN_HOST_TRIANGLES | LAGEN_HOST_X_ZEROED)) return fail(LAGEN_EINVAL, "unknown host flags");
-  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWSWEEP) return fail(LAGEN_EINVAL, "unknown engine");
+  if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWS_MIX) return fail(LAGEN_EINVAL, "unknown engine");
   if (eq < 0 || eq > 2) return fail(LAGEN_EINVAL, "unknown equation");
   if (batch < 0) return fail(LAGEN_EINVAL, "negative batch");
   int rc = validate(eq, stmts, nstmts);

@@ -14,7 +14,7 @@ struct RowsEntry {
   LaunchFn launch;
 };
 
-template <int N, int B, int WG, int NR = N>
+template <int N, int B, int WG, int NR = N, bool F4 = false>
 cudaError_t launch_rows_wg(const LaunchArgs& a, cudaStream_t s, int mode) {
   using P = cr::RPolicy<N, WG>;
   static std::atomic<unsigned long long> configured{0};
@@ -24,7 +24,7 @@ cudaError_t launch_rows_wg(const LaunchArgs& a, cudaStream_t s, int mode) {
   cudaError_t err = cudaGetDevice(&dev);
   if (err != cudaSuccess) return err;
   const unsigned long long bit = 1ull << (dev & 63);
-  auto kern = cr::chol_rows_kernel<N, B, WG, NR>;
+  auto kern = cr::chol_rows_kernel<N, B, WG, NR, F4>;
   if (!(configured.load(std::memory_order_acquire) & bit)) {
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM);
     if (err != cudaSuccess) return err;
@@ -82,6 +82,26 @@ cudaError_t launch_rows_pad(const LaunchArgs& a, cudaStream_t s) {
   if (wg == 2) return launch_rows_wg<N, 8, 2, NR>(a, s, mode);
   return launch_rows_wg<N, 8, 4, NR>(a, s, mode);
 }
+
+// n = 4 (mod 8), mixed blocks: a first 4 x 4 block row, then the b = 8
+// schedule (chol_rows.cuh, F4) — no padding, the problem's own footprint
+template <int N>
+cudaError_t launch_rows_mix(const LaunchArgs& a, cudaStream_t s) {
+  static const int mode = [] {
+    const char* e = std::getenv("LAGEN_ROWS_MODE");
+    return e ? std::atoi(e) : cr::mix_mode(N);
+  }();
+  static const int wg = [] {
+    const char* e = std::getenv("LAGEN_ROWS_WG");
+    return e ? std::atoi(e) : cr::mix_wg(N);
+  }();
+  if (wg == 1) return launch_rows_wg<N, 8, 1, N, true>(a, s, mode);
+  if (wg == 2) return launch_rows_wg<N, 8, 2, N, true>(a, s, mode);
+  return launch_rows_wg<N, 8, 4, N, true>(a, s, mode);
+}
+
+#define LAGEN_ROWS_MIX_ENTRY(N) \
+  { N, 4, 1, (int)cr::RPolicy<N, 2>::SMEM, &launch_rows_mix<N> }
 
 #define LAGEN_ROWS_PAD_ENTRY(NR, NP) \
   { NR, 4, 1, (int)cr::RPolicy<NP, 2>::SMEM, &launch_rows_pad<NR, NP> }

@@ -75,9 +75,27 @@ def _resolve(eq_name, n, variant, b, engine):
         if idx is not None and idx == pick["variant"] and table_engine != "auto":
             if b == pick["b"] or _lib.engine_supported(EQ_CODES[eq_name], n, b, idx, table_engine):
                 engine = table_engine
-    if engine not in _lib.ENGINES:
-        raise errors.UsageError(f"unknown engine {engine!r}; one of {sorted(_lib.ENGINES)}")
+    if engine not in _lib.ENGINES and engine != EMITTED:
+        raise errors.UsageError(f"unknown engine {engine!r}; one of {sorted(_lib.ENGINES) + [EMITTED]}")
     return stmts, idx, b, engine
+
+
+# engine "emitted": the statement list is emitted as its own size-specialised
+# CUDA kernel (emit.py, the counterpart of the reference's emit_function),
+# compiled with nvcc on first use and cached on disk and in the process
+EMITTED = "emitted"
+_emitted = {}
+
+
+def _emitted_kernel(eq_name, stmts, idx, n, b):
+    from . import emit
+    from .variants import stmts_key
+    key = (eq_name, stmts_key(stmts), n, b)
+    k = _emitted.get(key)
+    if k is None:
+        variant = builtin_variants(eq_name)[idx] if idx is not None else stmts
+        k = _emitted[key] = emit.compile_variant(eq_name, variant, n, b)
+    return k
 
 
 def _stream_ptr(stream):
@@ -128,14 +146,18 @@ def solve(eq, inputs, variant=None, b=None, out=None, info=None, stream=None, ch
         out = torch.empty((batch, n, n), dtype=torch.float64, device=dev)
     if info is None:
         info = torch.empty(batch, dtype=torch.int32, device=dev)
-    arr = _lib.stmt_array(stmts)
-    ptrs = (ctypes.c_void_p * 3)(*([t.data_ptr() for t in inputs] + [0] * (3 - len(inputs))))
-    with torch.cuda.device(dev):
-        rc = _lib.lib.lagen_b200_execute_engine(EQ_CODES[eq_name], ctypes.addressof(arr), len(stmts), n, b,
-                                                batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
-                                                ctypes.c_void_p(info.data_ptr()), _stream_ptr(stream),
-                                                _lib.ENGINES[engine])
-    _lib.check(rc, f"{eq_name} n={n} b={b} engine={engine}")
+    if engine == EMITTED:
+        with torch.cuda.device(dev):
+            _emitted_kernel(eq_name, stmts, idx, n, b).launch(inputs, out, info, stream)
+    else:
+        arr = _lib.stmt_array(stmts)
+        ptrs = (ctypes.c_void_p * 3)(*([t.data_ptr() for t in inputs] + [0] * (3 - len(inputs))))
+        with torch.cuda.device(dev):
+            rc = _lib.lib.lagen_b200_execute_engine(EQ_CODES[eq_name], ctypes.addressof(arr), len(stmts), n, b,
+                                                    batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
+                                                    ctypes.c_void_p(info.data_ptr()), _stream_ptr(stream),
+                                                    _lib.ENGINES[engine])
+        _lib.check(rc, f"{eq_name} n={n} b={b} engine={engine}")
     if check and batch:
         bad = torch.nonzero(info).flatten()
         if bad.numel():
@@ -170,8 +192,12 @@ class Plan:
                       ctypes.addressof(self._ptrs), ctypes.c_void_p(self.out.data_ptr()),
                       ctypes.c_void_p(self.info.data_ptr()))
         self.device = dev
+        self._kernel = _emitted_kernel(self.eq, stmts, idx, self.n, b) if engine == EMITTED else None
 
     def launch(self, stream=None):
+        if self._kernel is not None:
+            self._kernel.launch(self.inputs, self.out, self.info, stream)
+            return self.out
         rc = _lib.lib.lagen_b200_execute_engine(*self._args, _stream_ptr(stream), _lib.ENGINES[self.engine])
         _lib.check(rc, f"{self.eq} n={self.n} b={self.b}")
         return self.out

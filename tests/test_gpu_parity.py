@@ -42,7 +42,7 @@ def _cuda():
 
 
 # every engine of the C ABI (LAGEN_ENGINE_*), auto excluded
-ENGINES = ("generic", "warp", "column", "dataflow", "rows", "wave", "rowspad", "pipe", "rowsweep")
+ENGINES = ("generic", "warp", "column", "dataflow", "rows", "wave", "rowspad", "pipe", "rowsweep", "rowsmix")
 
 
 def blocks_of(n):
@@ -230,13 +230,13 @@ def test_non_spd_and_nan_are_reported():
     """info = first non-positive pivot + 1 (kernels.py:87-88) / -1 for NaN-Inf,
     on every engine that has the variant."""
     from paper_1906_08613_b200 import _lib
-    for n, bad in ((16, 6), (32, 20), (48, 37)):
+    for n, bad in ((16, 6), (32, 20), (44, 30), (48, 37)):
         A = executor.generate("cholesky", n, seed=1, batch=4)[0]
         A[2, bad, bad] = -1000.0
         with pytest.raises(errors.VerificationError):
             executor.solve("cholesky", [A], variant=2, b=4)
         for v in (1, 2):
-            for engine in ("generic", "warp", "column", "dataflow", "rows", "rowspad"):
+            for engine in ("generic", "warp", "column", "dataflow", "rows", "rowspad", "rowsmix"):
                 if not _lib.engine_supported(0, n, 4, v, engine):
                     continue
                 X, info = executor.solve("cholesky", [A], variant=v, b=4, check=False, engine=engine)

@@ -60,7 +60,7 @@ def main():
             # the reference's default blocks plus b = n (admissible: verify.py:232-233)
             blocks = sorted(set(default_blocks(n)) | {n})
             cands = [(v, b, e) for e in ("generic", "warp", "column", "dataflow", "rows", "wave", "rowspad",
-                                         "pipe", "rowsweep")
+                                         "pipe", "rowsweep", "rowsmix")
                      for v in builtin_variants(eq) for b in blocks
                      if _lib.engine_supported(_lib_eq(eq), n, b, v.index, e)
                      # rowsweep runs the same kernel for every variant (b = n): time one
