@@ -115,7 +115,9 @@ using emitted_var = Var<
 }}  // namespace eng
 }}  // namespace lagen
 
-extern "C" int {name}({params}, double* X, int* info, long long batch, void* stream) {{
+#define LAGEN_EMIT_API extern "C" __attribute__((visibility("default")))
+
+LAGEN_EMIT_API int {name}({params}, double* X, int* info, long long batch, void* stream) {{
   lagen::LaunchArgs a{{}};
   a.in[0] = {args[0]};
   a.in[1] = {args[1]};
@@ -127,7 +129,7 @@ extern "C" int {name}({params}, double* X, int* info, long long batch, void* str
   return (int)lagen::launch_warp<{EQ_CODES[eq]}, {n}, {b}, lagen::eng::emitted_var>(a, static_cast<cudaStream_t>(stream));
 }}
 
-extern "C" void {name}_shape(int* eq, int* n, int* b, int* nstmts) {{
+LAGEN_EMIT_API void {name}_shape(int* eq, int* n, int* b, int* nstmts) {{
   *eq = {EQ_CODES[eq]};
   *n = {n};
   *b = {b};
@@ -147,8 +149,14 @@ def compile_module(mod, out_dir=None, force=False):
     src = out_dir / f"{mod.name}.cu"
     src.write_text(mod.text)
     tmp = so.with_suffix(".tmp")
-    cmd = [_build.nvcc(), *_build.ARCH, *_build.NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-shared", "-cudart", "static",
-           str(src), "-o", str(tmp)]
+    # hidden visibility + no STB_GNU_UNIQUE: the module instantiates the same
+    # templates as liblagen_b200.so (and as other emitted modules); their
+    # function-local statics (per-kernel "configured" flags of launch_warp) and
+    # kernel stubs must stay private to each shared object — unique symbols are
+    # merged process-wide even under RTLD_LOCAL, and a module would then skip
+    # configuring its own copy of the kernel
+    cmd = [_build.nvcc(), *_build.ARCH, *_build.NVCC_FLAGS, "-Xcompiler", "-fvisibility=hidden,-fno-gnu-unique",
+           f"-I{INCLUDE}", f"-I{CSRC}", "-shared", "-cudart", "static", str(src), "-o", str(tmp)]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise errors.LagenError(f"nvcc failed on the emitted kernel {mod.name}:\n{proc.stderr[-2000:]}")
@@ -203,3 +211,14 @@ def compile_variant(eq, variant, n, b, out_dir=None):
     """emit -> nvcc -> load, for a live Algorithm / Variant / statement list."""
     mod = emit_cuda(eq, variant, n, b)
     return load(compile_module(mod, out_dir), mod)
+
+
+def prebuild(cases, out_dir=None, jobs=None):
+    """Emit and compile many (eq, variant, n, b) in parallel (each nvcc run is
+    a few seconds); returns the .so paths.  __graft_entry__.build() uses it so
+    the emitted-kernel parity tests find their modules in the in-tree cache."""
+    from concurrent.futures import ThreadPoolExecutor
+    mods = [emit_cuda(eq, v, n, b) for eq, v, n, b in cases]
+    jobs = jobs or max(1, min(len(mods), os.cpu_count() or 4))
+    with ThreadPoolExecutor(jobs) as ex:
+        return list(ex.map(lambda m: compile_module(m, out_dir), mods))

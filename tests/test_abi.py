@@ -122,3 +122,26 @@ def test_every_variant_has_a_generic_kernel_at_every_size():
             for b in default_blocks(n):
                 for v in builtin_variants(eq):
                     assert _lib.engine_supported(EQ_CODES[eq], n, b, v.index, "generic")
+
+
+def test_emitted_kernel_builds_and_exports(tmp_path):
+    """emit.py: a statement list -> one CUDA translation unit -> an sm_100a
+    shared object exporting <eq>_v<k>_n<n>_b<b>_cuda with the reference's
+    _signature order (codegen.py:143-152); no compute call without a GPU."""
+    import ctypes
+    from algorithm_fixtures import load
+    from paper_1906_08613_b200 import emit
+    cases, _ = load()
+    algs, inst, _ = cases["sylvester"]
+    mod = emit.emit_cuda("sylvester", algs[7], inst.n, 4)
+    assert mod.name == "sylvester_v7_n16_b4_cuda"
+    assert mod.text.count("    St<") == len(algs[7].statements)
+    assert "const double* L, const double* U, const double* C, double* X" in mod.text
+    so = emit.compile_module(mod, tmp_path)
+    lib = ctypes.CDLL(str(so))
+    assert hasattr(lib, mod.name)
+    vals = [ctypes.c_int() for _ in range(4)]
+    getattr(lib, mod.name + "_shape")(*[ctypes.byref(v) for v in vals])
+    assert [v.value for v in vals] == [2, 16, 4, len(algs[7].statements)]
+    with pytest.raises(Exception):
+        emit.emit_cuda("sylvester", algs[7], 16, 5)

@@ -380,6 +380,36 @@ def test_reference_algorithm_fixtures_drop_in():
                 assert np.linalg.norm(got[alg.output] - x) <= REL_TOL * max(1.0, np.linalg.norm(x))
 
 
+def test_emitted_kernels_from_algorithm_objects():
+    """f2: every synthesised variant emitted as its own compiled sm_100a kernel
+    (emit.py, the counterpart of codegen.emit_function) from the serialised
+    live `Algorithm` objects, against the reference interpreter's X for the
+    same variant and b; and through executor.solve(engine="emitted")."""
+    from concurrent.futures import ThreadPoolExecutor
+    from algorithm_fixtures import load
+    from paper_1906_08613_b200 import emit
+    cases, blocks = load()
+    jobs = [(name, alg, inst, b, want[(alg.index, b)][0])
+            for name, (algs, inst, want) in cases.items() for alg in algs for b in blocks]
+    with ThreadPoolExecutor(8) as ex:
+        kernels = list(ex.map(lambda j: emit.compile_variant(j[0], j[1], j[2].n, j[3]), jobs))
+    for (name, alg, inst, b, x), k in zip(jobs, kernels):
+        assert k.name == f"{name}_v{alg.index}_n{inst.n}_b{b}_cuda"
+        ins = [torch.from_numpy(np.ascontiguousarray(inst.bindings[nm], dtype=np.float64))[None].cuda()
+               for nm in EQ_INPUTS[name]]
+        X, info = k.solve(ins)
+        assert int(info[0]) == 0
+        assert np.linalg.norm(X[0].cpu().numpy() - x) <= REL_TOL * max(1.0, np.linalg.norm(x)), (name, alg.index, b)
+        X2, _ = executor.solve(name, ins, variant=alg, b=b, engine="emitted")
+        assert torch.equal(X2, X)
+    # a batch with a partial last round, at a size beyond the fixtures, against the generic engine
+    for name, v, n, b in (("sylvester", 7, 40, 8), ("lyapunov", 2, 36, 4), ("cholesky", 0, 64, 16)):
+        ins = executor.generate(name, n, seed=n, batch=1000)
+        X, _ = executor.solve(name, ins, variant=v, b=b, engine="emitted")
+        R, _ = executor.solve(name, ins, variant=v, b=b, engine="generic")
+        assert rel_diff(X.cpu().numpy(), R.cpu().numpy()).max() <= REL_TOL
+
+
 @pytest.mark.parametrize("eq", EQUATIONS)
 def test_config5_sampled(eq, oracle_mod):
     """BASELINE config 5 on one GPU: n = 64, 2^20 problems (2^32 doubles per
