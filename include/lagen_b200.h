@@ -42,6 +42,12 @@ extern "C" {
 
 #define LAGEN_B200_ABI_VERSION 1
 #define LAGEN_MAX_STMTS 16
+/* Sizes: 1 <= n <= 128 run on the size-specialised shared-memory engines;
+ * 128 < n <= LAGEN_BIG_MAX_N (b | n) run on the "big" engine (bigsolve.cu: the
+ * statement-list interpreter with X resident in its HBM output buffer, one
+ * problem per CTA) — the reference's interpreter has no size limit
+ * (verify.py:221-303), its generator stops at 128 (lowering.py:930-932). */
+#define LAGEN_BIG_MAX_N 1024
 
 /* equations (the three shipped cases, /root/reference/pkg/cases/ *.la) */
 enum {

@@ -24,6 +24,12 @@
 
 using namespace lagen;
 
+namespace lagen {
+// bigsolve.cu
+cudaError_t launch_big(const StmtList& sl, int eq, int n, int b, const double* const* in, double* X, int* info,
+                       long long batch, cudaStream_t s);
+}  // namespace lagen
+
 namespace {
 thread_local std::string g_last_error;
 }  // namespace
@@ -235,6 +241,11 @@ int check_common(int eq, int n, int b, long long batch, bool direct = false) {
   if (eq < 0 || eq > 2) return fail(LAGEN_EINVAL, "unknown equation");
   if (batch < 0) return fail(LAGEN_EINVAL, "negative batch");
   if (n < 1 || b < 1 || n % b) return fail(LAGEN_EUNSUPPORTED, "block size does not divide n");
+  if (n > 128) {  // the big engine (bigsolve.cu)
+    if (n > LAGEN_BIG_MAX_N)
+      return fail(LAGEN_EUNSUPPORTED, "n = " + std::to_string(n) + " exceeds LAGEN_BIG_MAX_N");
+    return LAGEN_OK;
+  }
   int bp = 0;
   if (!direct && !find_entry(eq, n, b) && !padded_size(eq, n, b, &bp))
     return fail(LAGEN_EUNSUPPORTED, "no sm_100a instance for (n=" + std::to_string(n) + ", b=" +
@@ -349,7 +360,9 @@ int lagen_b200_warp_supported(int eq, int n, int b, int variant) { return find_w
 
 int lagen_b200_engine_supported(int eq, int n, int b, int variant, int engine) {
   switch (engine) {
-    case LAGEN_ENGINE_GENERIC: return find_entry(eq, n, b) ? 1 : 0;
+    case LAGEN_ENGINE_GENERIC:
+      if (n > 128) return (n <= LAGEN_BIG_MAX_N && b >= 1 && n % b == 0 && eq >= 0 && eq <= 2) ? 1 : 0;
+      return find_entry(eq, n, b) ? 1 : 0;
     case LAGEN_ENGINE_WARP: return find_warp(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_COLUMN: return find_col(eq, n, b, variant) ? 1 : 0;
     case LAGEN_ENGINE_DATAFLOW: return 0;  // removed (never selected by the measured dispatch table)
@@ -393,6 +406,17 @@ int lagen_b200_execute_profile(int eq, const lagen_stmt* stmts, int nstmts, int 
   if (!inputs || !X) return fail(LAGEN_EINVAL, "null buffer");
   for (int i = 0; i < eq_ninputs(eq); ++i)
     if (!inputs[i]) return fail(LAGEN_EINVAL, "null input buffer");
+  if (n > 128) {  // beyond the shared-memory engines: X stays in HBM (bigsolve.cu)
+    if (engine != LAGEN_ENGINE_AUTO && engine != LAGEN_ENGINE_GENERIC)
+      return fail(LAGEN_EUNSUPPORTED, "n > 128 runs on the big engine only (engine auto or generic)");
+    StmtList sl;
+    std::memset(&sl, 0, sizeof(sl));
+    std::memcpy(sl.s, stmts, sizeof(lagen_stmt) * nstmts);
+    sl.count = nstmts;
+    cudaError_t berr = launch_big(sl, eq, n, b, inputs, X, info, batch, static_cast<cudaStream_t>(stream));
+    if (berr != cudaSuccess) return cuda_fail(berr, "big-engine launch");
+    return LAGEN_OK;
+  }
   if (!rs_direct && !find_entry(eq, n, b)) {  // identity-padded problem (see padded_size)
     int bp = 0;
     const int np = padded_size(eq, n, b, &bp);
@@ -705,7 +729,7 @@ int lagen_b200_execute_host_flags(int eq, const lagen_stmt* stmts, int nstmts, i
   // zero-copy triangles: every buffer must be mapped pinned memory and n even
   const double* mh_in[3] = {nullptr, nullptr, nullptr};
   double* mh_X = nullptr;
-  bool tri = (flags & LAGEN_HOST_TRIANGLES) && n % 2 == 0;
+  bool tri = (flags & LAGEN_HOST_TRIANGLES) && n % 2 == 0 && n <= 128;
   for (int i = 0; i < nin && tri; ++i) tri = (mh_in[i] = static_cast<const double*>(mapped(h_inputs[i]))) != nullptr;
   if (tri) tri = (mh_X = static_cast<double*>(const_cast<void*>(mapped(h_X)))) != nullptr;
   if ((flags & LAGEN_HOST_TRIANGLES) && !tri)

@@ -145,3 +145,16 @@ def test_emitted_kernel_builds_and_exports(tmp_path):
     assert [v.value for v in vals] == [2, 16, 4, len(algs[7].statements)]
     with pytest.raises(Exception):
         emit.emit_cuda("sylvester", algs[7], 16, 5)
+
+
+def test_big_engine_size_range():
+    """128 < n <= LAGEN_BIG_MAX_N (b | n) is served by the big engine
+    (bigsolve.cu) under engine auto / generic; nothing beyond it."""
+    big = int(re.search(r"#define LAGEN_BIG_MAX_N (\d+)", HEADER.read_text()).group(1))
+    assert big >= 256
+    for eq in EQUATIONS:
+        assert _lib.engine_supported(EQ_CODES[eq], 256, 16, 0, "generic")
+        assert _lib.engine_supported(EQ_CODES[eq], big, 8, 0, "generic")
+        assert not _lib.engine_supported(EQ_CODES[eq], big + 4, 4, 0, "generic")
+        assert not _lib.engine_supported(EQ_CODES[eq], 256, 7, 0, "generic")
+        assert not _lib.engine_supported(EQ_CODES[eq], 256, 8, 0, "warp")

@@ -411,6 +411,50 @@ def test_emitted_kernels_from_algorithm_objects():
 
 
 @pytest.mark.parametrize("eq", EQUATIONS)
+def test_sizes_beyond_128(eq, oracle_mod):
+    """f3: 128 < n <= LAGEN_BIG_MAX_N on the big engine (bigsolve.cu) — the
+    reference interpreter has no size limit (verify.py:221-303): every variant
+    x b in {4, 8, 16} at n = 144, the dispatch default at n = 132, 192, 256,
+    b = n, and the host path, against the oracle's run of the same (variant, b);
+    a non-SPD / NaN input is reported like at the small sizes."""
+    vs = builtin_variants(eq)
+    cases = [(144, v.index, b, 5) for v in vs for b in (4, 8, 16)]
+    cases += [(132, len(vs) - 1, 4, 3), (192, 1, 8, 700), (256, len(vs) - 1, 16, 3), (160, 0, 160, 2)]
+    for n, v, b, batch in cases:
+        host = oracle_mod.generate(eq, n, seed=n, first=0, batch=min(batch, 8))
+        if batch > 8:  # more problems than resident CTAs: the grid-stride loop
+            host = [np.concatenate([a] * (batch // 8 + 1))[:batch] for a in host]
+        ins = [torch.from_numpy(a).cuda() for a in host]
+        X, info = executor.solve(eq, ins, variant=v, b=b, check=False)
+        assert int((info != 0).sum()) == 0
+        k = min(batch, 8)
+        ref, rinfo = oracle_mod.execute(eq, vs[v].statements, n, b, [a[:k] for a in host])
+        assert (rinfo == 0).all()
+        got = X.cpu().numpy()
+        assert rel_diff(got[:k], ref).max() <= REL_TOL, (n, v, b)
+        if batch > 8:
+            assert np.array_equal(got, got[np.arange(batch) % 8])  # every round of the loop, same bits
+        res = oracle_mod.residual(eq, n, [a[:k] for a in host], got[:k])
+        assert res.max() <= 10 * n * EPS, (n, v, b, res.max() / (n * EPS))
+    n = 136
+    host = oracle_mod.generate(eq, n, seed=1, first=0, batch=3)
+    Xh, ih = executor.solve_host(eq, host, variant=0, b=8)
+    ref, _ = oracle_mod.execute(eq, vs[0].statements, n, 8, host)
+    assert rel_diff(np.asarray(Xh), ref).max() <= REL_TOL and int(np.abs(np.asarray(ih)).sum()) == 0
+    ins = [torch.from_numpy(a).cuda() for a in host]
+    if eq == "cholesky":
+        ins[0][1, 130, 130] = -1e6
+        want = [0, 131, 0]
+    else:
+        ins[-1][1, 3, 5] = float("nan")
+        want = [0, -1, 0]
+    _, info = executor.solve(eq, ins, variant=len(vs) - 1, b=8, check=False)
+    assert info.cpu().tolist() == want
+    with pytest.raises(errors.UnsupportedSizeError):
+        executor.solve(eq, [torch.zeros(1, 1028, 1028, dtype=torch.float64, device="cuda")] * len(ins), variant=0, b=4)
+
+
+@pytest.mark.parametrize("eq", EQUATIONS)
 def test_config5_sampled(eq, oracle_mod):
     """BASELINE config 5 on one GPU: n = 64, 2^20 problems (2^32 doubles per
     operand, past the 2^31-element line), seed 7; every problem's info, the
