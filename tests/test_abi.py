@@ -85,7 +85,7 @@ def test_rejects_bad_arguments_without_a_device():
     assert _execute(0, v, 16, 4, -1) == -1            # negative batch
     assert _execute(7, v, 16, 4, 1) == -1             # unknown equation
     assert _execute(0, v, 18, 4, 1) == -2             # b does not divide n
-    assert _execute(0, v, 132, 4, 1) == -2            # no instance
+    assert _execute(0, v, 1028, 4, 1) == -2           # beyond LAGEN_BIG_MAX_N (132 now runs on the big engine)
     assert _execute(0, [], 16, 4, 1) == -3            # empty statement list
     bad = [dict(s) for s in v]
     bad[0] = dict(bad[0], kind=9)
