@@ -527,14 +527,16 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
       for (int r = 0; r < 8; ++r) Pt[sw(r, c)] = -v[r];
       double* Xp = X + prob * NN;
       const int col = 8 * J + c;
-      if (col < N) {
+      // split roles: the updater warps stream the published tile to HBM during
+      // the next step (store_diag), off the solve -> hand-over critical path
+      if (MODE == 1 && col < N) {
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           bad = bad || !isfinite(v[r]);
           if (8 * I + r < N) __stcs(Xp + (long long)(8 * I + r) * N + col, v[r]);
         }
       }
-      if (EQ == 1 && I != J && 8 * J + c < N) {  // mirror tile (J, I): its row c is column c of this tile
+      if (MODE == 1 && EQ == 1 && I != J && 8 * J + c < N) {  // mirror tile (J, I): its row c is column c of this tile
         double* row = Xp + (long long)(8 * J + c) * N + 8 * I;
 #pragma unroll
         for (int mm = 0; mm < 4; ++mm)
@@ -542,6 +544,32 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
       }
     }
     if (sv == 0) stamp(4 * (d + 1) + 3);
+  };
+
+  // split roles: diagonal dd's published tiles (-X, swizzled) -> X in HBM, by
+  // the updater warps (tile i of the diagonal -> warp i mod NU; lane (g, t)
+  // stores row g, columns 2t, 2t + 1 as one 16-byte store; Lyapunov also the
+  // mirror tile's row g from column g of the tile).  Runs one step after the
+  // solve, behind the bulk updates.
+  auto store_diag = [&](int dd, long long prob, bool& bad) {
+    const int i0 = i0of(dd);
+    const int i1 = EQ == 2 ? (dd < T - 1 ? dd : T - 1) : dd / 2;
+    const double* pv = dbuf(dd);
+    double* Xp = X + prob * NN;
+    for (int I = i0 + w; I <= i1; I += NU) {
+      const int J = dd - I;
+      const double* Pt = pv + I * PS;
+      const double2 a = *reinterpret_cast<const double2*>(Pt + sw(g, 2 * t));
+      bad = bad || !isfinite(a.x) || !isfinite(a.y);
+      const int r = 8 * I + g, c = 8 * J + 2 * t;
+      if (r < N && c < N) __stcs(reinterpret_cast<double2*>(Xp + (long long)r * N + c), make_double2(-a.x, -a.y));
+      if (EQ == 1 && I != J) {
+        const int rm = 8 * J + g, cm = 8 * I + 2 * t;
+        if (rm < N && cm < N)
+          __stcs(reinterpret_cast<double2*>(Xp + (long long)rm * N + cm),
+                 make_double2(-Pt[sw(2 * t, g)], -Pt[sw(2 * t + 1, g)]));
+      }
+    }
   };
 
   // once: zero tile, the solve scratches' pad rows / pad columns (must read
@@ -580,9 +608,12 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
           sol_step(d, prob, bad);
         }
         upd_bulk(d, a0, a1);
+        if constexpr (MODE == 0)
+          if (d >= 1) store_diag(d - 1, prob, bad);
         if (w == 0) stamp(256 + 2 * (d + 1) + 1);
         gbar();
       }
+      if constexpr (MODE == 0) store_diag(2 * T - 2, prob, bad);
     } else {
       cp_async_wait<0>();
       gbar();
