@@ -107,7 +107,7 @@ struct PCfg {
   static constexpr int RMIN = MODE == 1 ? 128 : 96;
   static constexpr int fitb(int b) { return (b <= 1 || 65536 / (THREADS * b) >= RMIN) ? b : fitb(b - 1); }
   static constexpr int MINB_FIT = fitb(mn(smem_fit(PP), 2048 / THREADS));
-  static constexpr int kLyapMinb[17] = {1, 1, 1, 1, 7, 7, 6, 4, 4, 4, 2, 2, 2, 2, 2, 1, 1};
+  static constexpr int kLyapMinb[17] = {1, 1, 1, 1, 7, 7, 6, 4, 4, 3, 2, 2, 2, 2, 2, 1, 1};
   static constexpr int kSylvMinb[17] = {1, 1, 1, 1, 4, 4, 4, 3, 2, 2, 2, 1, 1, 1, 1, 1, 1};
   static constexpr int MINB_TAB = mn(EQ == 1 ? kLyapMinb[T] : kSylvMinb[T], mn(smem_fit(PP), 2048 / THREADS));
   static constexpr int MINB0 = (MODE == 1 || T < 4) ? MINB_FIT : MINB_TAB;

@@ -15,7 +15,7 @@ from pathlib import Path
 REPO = Path(__file__).resolve().parents[1]
 OUT = REPO / "gpurun_out"
 PROF = REPO / "profiles"
-FULL_ALL = [("chol128_rows_v1b8", "full_chol128"), ("chol92_rowspad_v1", "full_chol92"),
+FULL_ALL = [("chol128_rows_v1b8", "full_chol128"), ("chol92_rowsmix_v1", "full_chol92"),
         ("sylv128_pipe_v13", "full_sylv128"), ("lyap64_pipe_v5", "full_lyap64"),
         ("sylv64_pipe_v13", "full_sylv64"), ("lyap128_pipe_v5", "full_lyap128")]
 METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum",

@@ -18,7 +18,7 @@ run1() {  # name, run_one args
       python tools/run_one.py "$@" --reps 2 > $O/ncu_full_$name.log 2>&1; echo "full $name rc=$?"
 }
 KRE=chol_rows_kernel run1 chol128 --eq cholesky --n 128 --variant 1 --b 8 --engine rows
-KRE=chol_rows_kernel run1 chol92 --eq cholesky --n 92 --variant 1 --b 4 --engine rowspad
+KRE=chol_rows_kernel run1 chol92 --eq cholesky --n 92 --variant 1 --b 4 --engine rowsmix
 KRE=pipe_kernel run1 sylv128 --eq sylvester --n 128 --variant 13 --b 8 --engine pipe
 KRE=pipe_kernel run1 lyap64 --eq lyapunov --n 64 --variant 5 --b 8 --engine pipe
 KRE=pipe_kernel run1 sylv64 --eq sylvester --n 64 --variant 13 --b 8 --engine pipe
