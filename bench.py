@@ -307,9 +307,13 @@ def run_e2e(eq, plans, steps, world):
     d2h = sum(m[1] for m in moved)
 
     def one_pass():
+        # the sizes of a step are queued back to back (wait=False) and waited
+        # for once: the four-stream pipeline fills and drains once per step,
+        # not once per size
         for p, ins, out, info in hosts:
             executor.solve_host(eq, ins, variant=p.variant, b=p.b, out=out, info=info, engine=p.engine,
-                                out_zeroed=zeroed)
+                                out_zeroed=zeroed, wait=False)
+        executor.host_sync()
     one_pass()  # warm-up
     torch.cuda.synchronize()
     barrier(world)

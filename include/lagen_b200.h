@@ -192,9 +192,19 @@ int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, 
  *   LAGEN_HOST_X_ZEROED: the caller's X already holds zeros in its
  *     structurally-zero part (the reference's contract: "outputs must be
  *     zero-initialised by the caller", codegen.py:4-7); Cholesky then writes
- *     only X's upper triangle. */
+ *     only X's upper triangle.
+ *   LAGEN_HOST_ASYNC: return once the call's copies and launches are
+ *     queued; results (X, info) are valid after lagen_b200_host_sync().
+ *     Consecutive calls keep feeding the same four pipeline streams, so a
+ *     sequence of batches (e.g. a sweep over sizes) pays the pipeline's fill
+ *     and drain once instead of once per call.  The caller must keep every
+ *     host buffer alive and untouched until the sync; errors of queued work
+ *     are reported by the sync. */
 #define LAGEN_HOST_TRIANGLES 1
 #define LAGEN_HOST_X_ZEROED 2
+#define LAGEN_HOST_ASYNC 4
+/* Wait for all queued host-pipeline work of the current device. */
+int lagen_b200_host_sync(void);
 int lagen_b200_execute_host_flags(int eq, const lagen_stmt* stmts, int nstmts, int n, int b,
                                   long long batch, const double* const* h_inputs,
                                   double* h_X, int* h_info, int engine, int flags);

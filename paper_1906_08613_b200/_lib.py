@@ -49,6 +49,7 @@ def _load():
     lib.lagen_b200_host_bytes.argtypes = [i, i, ll, vp, vp]
     lib.lagen_b200_execute_host_flags.argtypes = [i, vp, i, i, i, ll, vp, vp, vp, i, i]
     lib.lagen_b200_host_bytes_flags.argtypes = [i, i, ll, i, vp, vp]
+    lib.lagen_b200_host_sync.argtypes = []
     lib.lagen_b200_cholesky.argtypes = [i, i, i, ll, vp, vp, vp, vp]
     lib.lagen_b200_lyapunov.argtypes = [i, i, i, ll, vp, vp, vp, vp, vp]
     lib.lagen_b200_sylvester.argtypes = [i, i, i, ll, vp, vp, vp, vp, vp, vp]
@@ -65,10 +66,11 @@ EXPORTED = (
     "lagen_b200_execute", "lagen_b200_execute_host", "lagen_b200_execute_host_engine", "lagen_b200_generate",
     "lagen_b200_execute_engine", "lagen_b200_warp_supported", "lagen_b200_engine_supported",
     "lagen_b200_execute_profile", "lagen_b200_host_bytes", "lagen_b200_execute_host_flags",
-    "lagen_b200_host_bytes_flags",
+    "lagen_b200_host_bytes_flags", "lagen_b200_host_sync",
 )
 HOST_TRIANGLES = 1
 HOST_X_ZEROED = 2
+HOST_ASYNC = 4
 ENGINES = {"auto": 0, "generic": 1, "warp": 2, "column": 3, "dataflow": 4, "rows": 5, "wave": 6, "rowspad": 7, "pipe": 8, "rowsweep": 9, "rowsmix": 10}
 
 

@@ -3,6 +3,7 @@
 // the seeded batched generator.  No C++ exception crosses the ABI.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -575,6 +576,7 @@ struct HostPipe {
   double* d_X[kNS] = {nullptr};
   int* d_info[kNS] = {nullptr};
   size_t cap_bytes = 0, cap_info = 0;
+  long long it = 0;  // chunks issued so far: chunk i runs on stream i mod kNS, across calls
   cudaError_t reserve(size_t bytes, size_t info_bytes) {
     if (bytes <= cap_bytes && info_bytes <= cap_info) return cudaSuccess;
     for (int k = 0; k < kNS; ++k) {
@@ -693,7 +695,9 @@ int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, 
 
 int lagen_b200_execute_host_flags(int eq, const lagen_stmt* stmts, int nstmts, int n, int b, long long batch,
                                   const double* const* h_inputs, double* h_X, int* h_info, int engine, int flags) {
-  if (flags & ~(LAGEN_HOST_TRIANGLES | LAGEN_HOST_X_ZEROED)) return fail(LAGEN_EINVAL, "unknown host flags");
+  if (flags & ~(LAGEN_HOST_TRIANGLES | LAGEN_HOST_X_ZEROED | LAGEN_HOST_ASYNC))
+    return fail(LAGEN_EINVAL, "unknown host flags");
+  const bool async = (flags & LAGEN_HOST_ASYNC) != 0;
   if (engine < LAGEN_ENGINE_AUTO || engine > LAGEN_ENGINE_ROWS_MIX) return fail(LAGEN_EINVAL, "unknown engine");
   if (eq < 0 || eq > 2) return fail(LAGEN_EINVAL, "unknown equation");
   if (batch < 0) return fail(LAGEN_EINVAL, "negative batch");
@@ -723,7 +727,10 @@ int lagen_b200_execute_host_flags(int eq, const lagen_stmt* stmts, int nstmts, i
   const Bands bd = host_bands(eq, n);
   std::lock_guard<std::mutex> lock(g_pipe_mu);
   HostPipe& hp = g_pipe[dev];
-  err = hp.reserve((size_t)chunk * prob_bytes, (size_t)chunk * sizeof(int));
+  // one capacity for every size (a chunk is <= 16 MiB per operand), so a
+  // sequence of calls never reallocates under queued work
+  err = hp.reserve(std::max((size_t)chunk * prob_bytes, (size_t)16 << 20),
+                   std::max((size_t)chunk * sizeof(int), (size_t)1 << 20));
   if (err != cudaSuccess) return cuda_fail(err, "host pipeline setup");
   if (chunk > batch) chunk = batch;
   // zero-copy triangles: every buffer must be mapped pinned memory and n even
@@ -750,8 +757,8 @@ int lagen_b200_execute_host_flags(int eq, const lagen_stmt* stmts, int nstmts, i
       tri_copy_kernel<<<(unsigned)grid, 512, 0, st>>>(src, dst, cnt, n, parts[part]);
       return cudaGetLastError();
     };
-    for (long long c0 = 0, it = 0; status == LAGEN_OK && c0 < batch; c0 += chunk, ++it) {
-      const int k = (int)(it % kNS);
+    for (long long c0 = 0; status == LAGEN_OK && c0 < batch; c0 += chunk) {
+      const int k = (int)(hp.it++ % kNS);
       const long long cnt = (batch - c0) < chunk ? (batch - c0) : chunk;
       for (int i = 0; i < nin && err == cudaSuccess; ++i)
         err = tcopy(mh_in[i] + c0 * n * n, hp.d_in[k][i], cnt, input_part(eq, i), hp.st[k]);
@@ -765,7 +772,7 @@ int lagen_b200_execute_host_flags(int eq, const lagen_stmt* stmts, int nstmts, i
         err = cudaMemcpyAsync(h_info + c0, hp.d_info[k], cnt * sizeof(int), cudaMemcpyDeviceToHost, hp.st[k]);
       if (err != cudaSuccess) { status = cuda_fail(err, "triangle scatter"); break; }
     }
-    for (int k = 0; k < kNS; ++k) {
+    for (int k = 0; k < kNS && (!async || status != LAGEN_OK); ++k) {
       cudaError_t e2 = cudaStreamSynchronize(hp.st[k]);
       if (e2 != cudaSuccess && status == LAGEN_OK) status = cuda_fail(e2, "host pipeline sync");
     }
@@ -804,8 +811,8 @@ int lagen_b200_execute_host_flags(int eq, const lagen_stmt* stmts, int nstmts, i
     return cudaSuccess;
   };
   int status = LAGEN_OK;
-  for (long long c0 = 0, it = 0; status == LAGEN_OK && c0 < batch; c0 += chunk, ++it) {
-    const int k = (int)(it % kNS);
+  for (long long c0 = 0; status == LAGEN_OK && c0 < batch; c0 += chunk) {
+    const int k = (int)(hp.it++ % kNS);
     const long long cnt = (batch - c0) < chunk ? (batch - c0) : chunk;
     for (int i = 0; i < nin && err == cudaSuccess; ++i)
       err = copy(hp.d_in[k][i], h_inputs[i] + c0 * n * n, cnt, cudaMemcpyHostToDevice, hp.st[k]);
@@ -819,11 +826,27 @@ int lagen_b200_execute_host_flags(int eq, const lagen_stmt* stmts, int nstmts, i
       err = cudaMemcpyAsync(h_info + c0, hp.d_info[k], cnt * sizeof(int), cudaMemcpyDeviceToHost, hp.st[k]);
     if (err != cudaSuccess) { status = cuda_fail(err, "D2H"); break; }
   }
-  for (int k = 0; k < kNS; ++k) {
+  for (int k = 0; k < kNS && (!async || status != LAGEN_OK); ++k) {
     cudaError_t e2 = cudaStreamSynchronize(hp.st[k]);
     if (e2 != cudaSuccess && status == LAGEN_OK) status = cuda_fail(e2, "host pipeline sync");
   }
   for (auto& th : fill) th.join();
+  return status;
+}
+
+int lagen_b200_host_sync(void) {
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return cuda_fail(err, "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return fail(LAGEN_EINVAL, "device index out of range");
+  std::lock_guard<std::mutex> lock(g_pipe_mu);
+  HostPipe& hp = g_pipe[dev];
+  int status = LAGEN_OK;
+  for (int k = 0; k < kNS; ++k) {
+    if (!hp.st[k]) continue;
+    cudaError_t e2 = cudaStreamSynchronize(hp.st[k]);
+    if (e2 != cudaSuccess && status == LAGEN_OK) status = cuda_fail(e2, "host pipeline sync");
+  }
   return status;
 }
 

@@ -239,8 +239,19 @@ def interpret_algorithm(alg, inst, b, on_iteration=None):
     return {alg.output: X[0].cpu().numpy()}, flop_count(eq_name, stmts, n, b)
 
 
+_pending_host = []  # host buffers of queued wait=False calls, kept alive until host_sync()
+
+
+def host_sync():
+    """Wait for every queued `solve_host(..., wait=False)` call of the current
+    device (lagen_b200_host_sync); their X / info are valid afterwards."""
+    rc = _lib.lib.lagen_b200_host_sync()
+    _pending_host.clear()
+    _lib.check(rc, "host pipeline sync")
+
+
 def solve_host(eq, inputs, variant=None, b=None, out=None, info=None, engine=None, triangles=None,
-               out_zeroed=False):
+               out_zeroed=False, wait=True):
     """Host buffers (numpy arrays or CPU tensors, ideally pinned) -> host X.
     Streams the batch through the GPU with transfer / solve overlap; runs the
     same kernel as solve() (dispatch-table engine unless given).
@@ -253,7 +264,10 @@ def solve_host(eq, inputs, variant=None, b=None, out=None, info=None, engine=Non
     caller-zeroed X at n >= 48, Lyapunov at n >= 64; pinned buffers, even n.  out_zeroed: `out`
     already holds zeros in X's structurally-zero part — the reference's own
     contract for its emitted kernels (codegen.py:4-7) — so Cholesky writes
-    only X's upper triangle (LAGEN_HOST_X_ZEROED)."""
+    only X's upper triangle (LAGEN_HOST_X_ZEROED).  wait=False queues the
+    call and returns (LAGEN_HOST_ASYNC): a sequence of batches then shares one
+    pipeline fill / drain; call host_sync() before reading X or info and keep
+    the input buffers untouched until then."""
     eq_name = _eq_name(eq)
     if out_zeroed and out is None:
         raise errors.UsageError("out_zeroed needs a caller-provided out buffer")
@@ -292,7 +306,10 @@ def solve_host(eq, inputs, variant=None, b=None, out=None, info=None, engine=Non
     if triangles is None:
         wins = (eq_name == "cholesky" and out_zeroed and n >= 48) or (eq_name == "lyapunov" and n >= 64)
         triangles = wins and n % 2 == 0 and all(a.is_pinned() for a in arrs) and out.is_pinned()
-    flags = (_lib.HOST_TRIANGLES if triangles else 0) | (_lib.HOST_X_ZEROED if out_zeroed else 0)
+    flags = ((_lib.HOST_TRIANGLES if triangles else 0) | (_lib.HOST_X_ZEROED if out_zeroed else 0)
+             | (0 if wait else _lib.HOST_ASYNC))
+    if not wait:
+        _pending_host.append((arrs, out, info))
     rc = _lib.lib.lagen_b200_execute_host_flags(EQ_CODES[eq_name], ctypes.addressof(arr), len(stmts), n, b,
                                                 batch, ctypes.addressof(ptrs), ctypes.c_void_p(out.data_ptr()),
                                                 ctypes.c_void_p(info.data_ptr()), _lib.ENGINES[engine], flags)

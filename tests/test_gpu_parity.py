@@ -454,6 +454,27 @@ def test_sizes_beyond_128(eq, oracle_mod):
         executor.solve(eq, [torch.zeros(1, 1028, 1028, dtype=torch.float64, device="cuda")] * len(ins), variant=0, b=4)
 
 
+def test_host_pipeline_async_sequence():
+    """solve_host(..., wait=False): several batches of different sizes and
+    equations queued back to back on the same pipeline streams, one
+    host_sync(); every result equals the device path bit for bit."""
+    jobs = []
+    for eq, n, batch in (("cholesky", 64, 3000), ("sylvester", 24, 5000), ("lyapunov", 96, 900),
+                         ("cholesky", 12, 20000), ("cholesky", 100, 700)):
+        ins = executor.generate(eq, n, seed=n, batch=batch)
+        want, _ = executor.solve(eq, ins)
+        host = [t.cpu().pin_memory() for t in ins]
+        out = torch.zeros((batch, n, n), dtype=torch.float64).pin_memory()
+        info = torch.full((batch,), 7, dtype=torch.int32).pin_memory()
+        executor.solve_host(eq, host, out=out, info=info, out_zeroed=eq == "cholesky", wait=False)
+        jobs.append((want.cpu(), out, info))
+    executor.host_sync()
+    for want, out, info in jobs:
+        assert torch.equal(out, want)
+        assert int(info.abs().sum()) == 0
+    executor.host_sync()  # idempotent
+
+
 @pytest.mark.parametrize("eq", EQUATIONS)
 def test_config5_sampled(eq, oracle_mod):
     """BASELINE config 5 on one GPU: n = 64, 2^20 problems (2^32 doubles per
