@@ -14,9 +14,9 @@
 // problem, lane r = row r; 32 / LP problems per warp run in lockstep.  Lane r
 // keeps row r of the right-hand side / solution in registers (y[0..n-1],
 // static indices), so the X U part of every column is lane-local; the forward
-// substitution down column c is n steps of (x_k = y_k / (l_kk + u_cc) in lane
-// k, shuffled to the group, y_r -= l_rk x_k): the dependent chain per step is
-// DMUL -> SHFL -> DFMA.  L is staged in shared memory as a square with a zero
+// substitution down column c is n steps of (x_k in lane k, shuffled to the
+// group, z_r -= (l_rk piv_r) x_k on the pivot-scaled value z_r = piv_r y_r):
+// the dependent chain per step is SHFL -> DFMA.  L is staged in shared memory as a square with a zero
 // upper triangle and zero diagonal (lane r reads l_rk at a per-lane base plus a
 // compile-time offset; pitch n + 1 keeps the lanes on distinct banks); U's
 // rows are read as broadcasts (Sylvester: packed upper rows; Lyapunov: the
@@ -51,10 +51,23 @@ struct RCfg {
   static constexpr int PSZ = (LSQ + UPK + 1) & ~1;                         // doubles per problem (16 B aligned)
   static constexpr int THREADS = W * 32;
   static constexpr size_t SMEM = (size_t)W * PPW * PSZ * 8;
+  // CTAs per SM and the substitution form, measured per (equation, n) over
+  // MINB in 2..8 x {scaled, unscaled} at the BASELINE batches
+  // (tools/experiments/rsw_bench.cu, profiles/r02_rowsweep_sweep.txt): more
+  // CTAs hide the substitution chain's latency even where the row of y then
+  // spills a few registers; the scaled form (a DFMA less on the chain, n - 1
+  // more products live) wins where registers allow.  Index n / 4.
   static constexpr int mn(int a, int b) { return a < b ? a : b; }
-  // CTAs per SM: shared memory, threads, and >= 128 registers (row of y)
+  static constexpr int kMinb[2][9] = {{0, 8, 8, 5, 4, 3, 5, 4, 3}, {0, 8, 8, 6, 5, 5, 5, 4, 4}};
+  static constexpr bool kScaled[2][9] = {{0, 0, 0, 1, 1, 1, 0, 0, 1}, {0, 0, 0, 1, 0, 0, 0, 0, 0}};
   static constexpr int RMIN = N > 16 ? 168 : N > 8 ? 96 : 64;
-  static constexpr int MINB0 = mn(mn((227 * 1024) / (int)SMEM, 2048 / THREADS), 65536 / (THREADS * RMIN));
+  static constexpr int MINB_FIT = mn(mn((227 * 1024) / (int)SMEM, 2048 / THREADS), 65536 / (THREADS * RMIN));
+  static constexpr int MINB0 = N % 4 == 0 ? mn(kMinb[EQ - 1][N / 4], mn((227 * 1024) / (int)SMEM, 2048 / THREADS)) : MINB_FIT;
+#ifdef LAGEN_RSW_SCALED
+  static constexpr bool SCALED = LAGEN_RSW_SCALED;
+#else
+  static constexpr bool SCALED = N % 4 == 0 ? kScaled[EQ - 1][N / 4] : false;
+#endif
 #ifdef LAGEN_RSW_MINB
   static constexpr int MINB = LAGEN_RSW_MINB;
 #else
@@ -117,13 +130,28 @@ __global__ void __launch_bounds__(RCfg<EQ, N>::THREADS, RCfg<EQ, N>::MINB)
       // u_cc: Sylvester U(c, c); Lyapunov L(c, c) (read from global, cached)
       const double ucc = EQ == 2 ? Us[urow(N, c)] : __ldg(Lp + (long long)c * N + c);
       const double piv = real ? recip(lrr + ucc) : 0.0;
-      // forward substitution down column c
+      // forward substitution down column c.  SCALED: on the pivot-scaled
+      // value z_r = piv_r (y_r - sum_k l_rk x_k) — lane k's z is x_k itself,
+      // so the dependent chain per step is SHFL -> DFMA (the scaling
+      // l_rk piv_r is off the chain); otherwise DMUL -> SHFL -> DFMA on y
+      // (fewer live registers: measured per size, RCfg::SCALED)
+      double x;
+      if constexpr (P::SCALED) {
+        double z = y[c] * piv;
 #pragma unroll
-      for (int k = 0; k < N - 1; ++k) {
-        const double xk = __shfl_sync(0xffffffffu, y[c] * piv, gbase + k);
-        y[c] = fma(-lr[k], xk, y[c]);
+        for (int k = 0; k < N - 1; ++k) {
+          const double xk = __shfl_sync(0xffffffffu, z, gbase + k);
+          z = fma(-(lr[k] * piv), xk, z);
+        }
+        x = z;
+      } else {
+#pragma unroll
+        for (int k = 0; k < N - 1; ++k) {
+          const double xk = __shfl_sync(0xffffffffu, y[c] * piv, gbase + k);
+          y[c] = fma(-lr[k], xk, y[c]);
+        }
+        x = y[c] * piv;
       }
-      const double x = y[c] * piv;
       y[c] = x;
       bad = bad || !isfinite(x);
       // push into the later columns: y_c' -= x u_{c,c'}
