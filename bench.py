@@ -285,9 +285,10 @@ def run_e2e(eq, plans, steps, world):
     """Same workload through the public host-buffer API (executor.solve_host):
     every step moves the inputs from pinned host memory to the GPU, solves,
     and moves X and info back.  Only the structurally needed part of each
-    operand crosses PCIe where that wins (solve_host's default: zero-copy
-    triangles for Cholesky n >= 48 and Lyapunov n >= 64, dense copies
-    elsewhere); for Cholesky the host X is zeroed once at allocation — the
+    operand crosses PCIe where that wins (solve_host's default from n = 16
+    on: the copy engines move the contiguous mostly-needed half of each
+    triangular operand, zero-copy kernels the remaining small triangle; dense
+    copies below); for Cholesky the host X is zeroed once at allocation — the
     reference's own contract for its kernels' outputs (codegen.py:4-7) — so
     only X's upper triangle comes back there (LAGEN_HOST_X_ZEROED)."""
     from paper_1906_08613_b200 import _lib, executor
@@ -300,8 +301,8 @@ def run_e2e(eq, plans, steps, world):
         info = torch.empty(p.batch, dtype=torch.int32).pin_memory()
         hosts.append((p, ins, out, info))
     def flags_of(n):  # what solve_host's default picks (executor.solve_host, triangles=None)
-        tri = (eq == "cholesky" and n >= 48) or (eq == "lyapunov" and n >= 64)
-        return (_lib.HOST_TRIANGLES if tri and n % 2 == 0 else 0) | (_lib.HOST_X_ZEROED if zeroed else 0)
+        tri = executor.host_triangles_default(eq, n)
+        return (_lib.HOST_TRIANGLES if tri else 0) | (_lib.HOST_X_ZEROED if zeroed else 0)
     moved = [_lib.host_bytes(EQ_CODES[eq], p.n, p.batch, flags_of(p.n)) for p, _, _, _ in hosts]
     h2d = sum(m[0] for m in moved)
     d2h = sum(m[1] for m in moved)

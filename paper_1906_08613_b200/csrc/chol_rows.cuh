@@ -34,6 +34,9 @@
 #ifndef LAGEN_ROWS_MAXW
 #define LAGEN_ROWS_MAXW 16
 #endif
+#ifndef LAGEN_ROWS_PCAP
+#define LAGEN_ROWS_PCAP 16  // problems per CTA cap (group barriers 1..P, per-group flags: <= 32 with WG = 1)
+#endif
 // Loads / stores walk warp-per-row when a row's 16-byte pairs fill whole
 // warps, and from this many pairs per row on (the partial second pass idles
 // fewer lanes than the flattened loop's per-element division costs: 4-5 %
@@ -72,7 +75,7 @@ struct RPolicy {
   static constexpr int S2 = BUDGET / (2 * SLOT * 8 + 640);
   static constexpr int DB = S2 >= LAGEN_ROWS_DBMIN ? 2 : 1;
   static constexpr int P0 = DB == 2 ? S2 : (S1 < 1 ? 1 : S1);
-  static constexpr int PMAX = LAGEN_ROWS_MAXW / WG > 16 ? 16 : LAGEN_ROWS_MAXW / WG;  // warps per CTA cap
+  static constexpr int PMAX = LAGEN_ROWS_MAXW / WG > LAGEN_ROWS_PCAP ? LAGEN_ROWS_PCAP : LAGEN_ROWS_MAXW / WG;  // warps per CTA cap
   static constexpr int P = P0 > PMAX ? PMAX : P0;
   static constexpr int WARPS = P * WG;
   static constexpr int RSB = 16 + 64;

@@ -627,22 +627,38 @@ struct TriRows {
   int start[130];
   int col0[129];
 };
+// A per-unit offset table (16-byte units inside one problem) is built in
+// shared memory once per CTA; every thread then keeps four independent
+// 16-byte transfers in flight (PCIe reads are latency-bound per request).
 __global__ void tri_copy_kernel(const double* __restrict__ src, double* __restrict__ dst, long long cnt, int n,
                                 const __grid_constant__ TriRows tr) {
-  const int U = tr.start[n];  // units per problem
-  const long long total = cnt * U;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += stride) {
-    const long long p = i / U;
-    const int u = (int)(i - p * U);
-    int lo = 0, hi = n - 1;  // last row with start <= u
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (tr.start[mid] <= u) lo = mid;
-      else hi = mid - 1;
+  extern __shared__ unsigned short tri_tab[];  // unit u -> (row * n + column) / 2
+  const int U = tr.start[n];                   // units per problem
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    const int base = (r * n + tr.col0[r]) >> 1;
+    for (int u = tr.start[r]; u < tr.start[r + 1]; ++u) tri_tab[u] = (unsigned short)(base + (u - tr.start[r]));
+  }
+  __syncthreads();
+  const double2* __restrict__ s2 = reinterpret_cast<const double2*>(src);
+  double2* __restrict__ d2 = reinterpret_cast<double2*>(dst);
+  const long long total = cnt * U, nn2 = (long long)n * n / 2;
+  const long long step = (long long)gridDim.x * 4 * blockDim.x;
+  for (long long i0 = (long long)blockIdx.x * 4 * blockDim.x + threadIdx.x; i0 < total; i0 += step) {
+    double2 v[4];
+    long long off[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const long long i = i0 + (long long)k * blockDim.x;
+      off[k] = -1;
+      if (i < total) {
+        const long long p = i / U;
+        off[k] = p * nn2 + tri_tab[(int)(i - p * U)];
+        v[k] = s2[off[k]];
+      }
     }
-    const long long off = (p * n + lo) * n + tr.col0[lo] + 2 * (u - tr.start[lo]);
-    *reinterpret_cast<double2*>(dst + off) = *reinterpret_cast<const double2*>(src + off);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (off[k] >= 0) d2[off[k]] = v[k];
   }
 }
 TriRows tri_rows(int part, int n) {
@@ -653,6 +669,50 @@ TriRows tri_rows(int part, int n) {
     part_cols(part, n, r, &c0, &c1);
     t.col0[r] = c0;
     t.start[r + 1] = t.start[r] + (c1 - c0) / 2;
+  }
+  return t;
+}
+long long part_doubles(int part, int n);
+// Hybrid transfer of a triangular part: the half of the rows that is mostly
+// needed goes through the copy engines as ONE strided copy per chunk — rows
+// [0, s) (upper part) or [s, n) (lower part) of a row-major matrix are
+// contiguous, s n doubles per problem, so the 2-D copy has one long row per
+// problem — and only the remaining small triangle (rows [s, n) of an upper
+// part, rows [0, s) of a lower part) goes through the zero-copy kernel.
+// Measured (tools/e2e_probe4.py): the copy engines move 45 GB/s each way
+// under bidirectional load, the zero-copy kernels 25, so the bulk belongs on
+// the engines.  s = n / 2 rounded down to the 8-column tile grid; 0 (no
+// split) below n = 16.  LAGEN_HOST_SPLIT=0 restores all-zero-copy triangles.
+int split_row(int n) {
+  static const int on = [] {
+    const char* e = std::getenv("LAGEN_HOST_SPLIT");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (!on || n < 16) return 0;
+  return (n / 2) & ~7;
+}
+// rows [ra, rb) of a part only
+TriRows tri_rows_range(int part, int n, int ra, int rb) {
+  TriRows t;
+  t.start[0] = 0;
+  for (int r = 0; r < n; ++r) {
+    int c0, c1;
+    part_cols(part, n, r, &c0, &c1);
+    if (r < ra || r >= rb) c1 = c0;
+    t.col0[r] = c0;
+    t.start[r + 1] = t.start[r] + (c1 - c0) / 2;
+  }
+  return t;
+}
+// doubles per problem a part moves over PCIe with the split at row s
+long long part_doubles_split(int part, int n, int s) {
+  if (part == 0) return (long long)n * n;
+  if (s <= 0) return part_doubles(part, n);
+  long long t = part == 1 ? (long long)s * n : (long long)(n - s) * n;  // the engine-copied rows, full width
+  for (int r = (part == 1 ? s : 0); r < (part == 1 ? n : s); ++r) {
+    int c0, c1;
+    part_cols(part, n, r, &c0, &c1);
+    t += c1 - c0;
   }
   return t;
 }
@@ -749,12 +809,31 @@ int lagen_b200_execute_host_flags(int eq, const lagen_stmt* stmts, int nstmts, i
       Reserve() { t_sm_reserve = 8; }
       ~Reserve() { t_sm_reserve = 0; }
     } reserve_guard;
-    TriRows parts[3] = {tri_rows(0, n), tri_rows(1, n), tri_rows(2, n)};
+    const int sp = split_row(n);
+    // zero-copy regions: the whole part without a split; with it, rows [sp, n)
+    // of an upper part and rows [0, sp) of a lower part
+    TriRows parts[3] = {tri_rows(0, n), sp ? tri_rows_range(1, n, sp, n) : tri_rows(1, n),
+                        sp ? tri_rows_range(2, n, 0, sp) : tri_rows(2, n)};
+    // one operand chunk: engine copy of the contiguous half (or of a full
+    // part), then the zero-copy kernel for the remaining rows; both on stream
+    // st.  src / dst are a mapped-host and a device pointer (either order;
+    // unified addressing lets the engines resolve the direction).
     auto tcopy = [&](const double* src, double* dst, long long cnt, int part, cudaStream_t st) {
+      if (part == 0) return cudaMemcpyAsync(dst, src, (size_t)cnt * prob_bytes, cudaMemcpyDefault, st);
+      if (sp) {
+        const size_t row0 = part == 1 ? 0 : (size_t)sp * n;  // first engine-copied element
+        const size_t width = (part == 1 ? (size_t)sp : (size_t)(n - sp)) * n * sizeof(double);
+        cudaError_t e = cudaMemcpy2DAsync(dst + row0, prob_bytes, src + row0, prob_bytes, width, (size_t)cnt,
+                                          cudaMemcpyDefault, st);
+        if (e != cudaSuccess) return e;
+      }
       const long long units = cnt * parts[part].start[n];
-      long long grid = (units + 511) / 512;
-      if (grid > 32) grid = 32;  // 32 CTAs x 512 threads keep PCIe busy (tools/zc_probe.cu)
-      tri_copy_kernel<<<(unsigned)grid, 512, 0, st>>>(src, dst, cnt, n, parts[part]);
+      if (units == 0) return cudaSuccess;
+      long long grid = (units + 2047) / 2048;
+      if (grid > 32) grid = 32;  // 32 CTAs x 512 threads x 4 transfers keep PCIe busy (tools/zc_probe.cu)
+      if (grid < 1) grid = 1;
+      tri_copy_kernel<<<(unsigned)grid, 512, (size_t)parts[part].start[n] * sizeof(unsigned short), st>>>(
+          src, dst, cnt, n, parts[part]);
       return cudaGetLastError();
     };
     for (long long c0 = 0; status == LAGEN_OK && c0 < batch; c0 += chunk) {
@@ -854,10 +933,11 @@ int lagen_b200_host_bytes_flags(int eq, int n, long long batch, int flags, long 
   if (!(flags & LAGEN_HOST_TRIANGLES) || n % 2) return lagen_b200_host_bytes(eq, n, batch, h2d, d2h);
   if (eq < 0 || eq > 2 || n < 1 || batch < 0) return fail(LAGEN_EINVAL, "bad arguments");
   long long in = 0;
-  for (int i = 0; i < eq_ninputs(eq); ++i) in += part_doubles(input_part(eq, i), n);
+  const int sp = n <= 128 ? split_row(n) : 0;
+  for (int i = 0; i < eq_ninputs(eq); ++i) in += part_doubles_split(input_part(eq, i), n, sp);
   const int xpart = (eq == LAGEN_CHOLESKY && (flags & LAGEN_HOST_X_ZEROED)) ? 1 : 0;
   if (h2d) *h2d = batch * in * (long long)sizeof(double);
-  if (d2h) *d2h = batch * (part_doubles(xpart, n) * (long long)sizeof(double) + (long long)sizeof(int));
+  if (d2h) *d2h = batch * (part_doubles_split(xpart, n, sp) * (long long)sizeof(double) + (long long)sizeof(int));
   return LAGEN_OK;
 }
 

@@ -239,6 +239,15 @@ def interpret_algorithm(alg, inst, b, on_iteration=None):
     return {alg.output: X[0].cpu().numpy()}, flop_count(eq_name, stmts, n, b)
 
 
+def host_triangles_default(eq_name, n):
+    """Whether solve_host moves triangles only by default: measured per n
+    (tools/e2e_probe4.py, profiles/r02_e2e_hybrid.txt) the hybrid transfer —
+    copy engines for the contiguous mostly-needed half of each triangular
+    operand, zero-copy kernels for the remaining small triangle — beats dense
+    copies from n = 16 on for all three equations (n even, n <= 128)."""
+    return 16 <= n <= 128 and n % 2 == 0
+
+
 _pending_host = []  # host buffers of queued wait=False calls, kept alive until host_sync()
 
 
@@ -258,10 +267,11 @@ def solve_host(eq, inputs, variant=None, b=None, out=None, info=None, engine=Non
 
     triangles: move only the structurally needed part of each operand over
     PCIe (zero-copy kernels on the mapped pinned buffers, LAGEN_HOST_TRIANGLES).
-    Zero-copy transfers reach ~37 GB/s each way against ~50 for the copy
-    engines' dense copies (tools/zc_probe.cu), so the default (None) uses them
-    only where the byte saving wins (tools/e2e_tri_probe.py): Cholesky with a
-    caller-zeroed X at n >= 48, Lyapunov at n >= 64; pinned buffers, even n.  out_zeroed: `out`
+    The copy engines move the contiguous, mostly-needed half of the rows of
+    each triangular operand (one strided copy per chunk) and zero-copy kernels
+    the remaining small triangle (the engines sustain ~45 GB/s each way under
+    bidirectional load, the kernels ~25); the default (None) does this from
+    n = 16 on (host_triangles_default; pinned buffers, even n).  out_zeroed: `out`
     already holds zeros in X's structurally-zero part — the reference's own
     contract for its emitted kernels (codegen.py:4-7) — so Cholesky writes
     only X's upper triangle (LAGEN_HOST_X_ZEROED).  wait=False queues the
@@ -304,8 +314,8 @@ def solve_host(eq, inputs, variant=None, b=None, out=None, info=None, engine=Non
     arr = _lib.stmt_array(stmts)
     ptrs = (ctypes.c_void_p * 3)(*([t.data_ptr() for t in arrs] + [0] * (3 - len(arrs))))
     if triangles is None:
-        wins = (eq_name == "cholesky" and out_zeroed and n >= 48) or (eq_name == "lyapunov" and n >= 64)
-        triangles = wins and n % 2 == 0 and all(a.is_pinned() for a in arrs) and out.is_pinned()
+        triangles = (host_triangles_default(eq_name, n) and all(a.is_pinned() for a in arrs)
+                     and out.is_pinned())
     flags = ((_lib.HOST_TRIANGLES if triangles else 0) | (_lib.HOST_X_ZEROED if out_zeroed else 0)
              | (0 if wait else _lib.HOST_ASYNC))
     if not wait:

@@ -14,3 +14,5 @@ bash tools/evidence.sh
 for w in c1 c5-chol c5-lyap c5-sylv; do
   timeout 900 python bench.py --workload $w --steps 5 --warmup 3 --no-cpu > $O/bench_$w.log 2>&1; echo "$w rc=$?"
 done
+for eq in cholesky lyapunov sylvester; do timeout 300 python tools/e2e_probe4.py $eq; done > $O/e2e_hybrid.txt 2>&1; echo "e2e probe rc=$?"
+LAGEN_HOST_SPLIT=0 timeout 300 python tools/e2e_probe4.py cholesky > $O/e2e_nosplit.txt 2>&1
