@@ -185,10 +185,13 @@ int lagen_b200_execute_host_engine(int eq, const lagen_stmt* stmts, int nstmts, 
 
 /* Same with flags:
  *   LAGEN_HOST_TRIANGLES: move only the structurally needed part of every
- *     operand over PCIe — zero-copy kernels read A / S / U's upper and L's
- *     lower triangles (rows rounded to 8-column tiles) straight from mapped
- *     pinned host memory and write X back the same way.  Needs pinned
- *     (cudaHostAlloc / cudaHostRegister-mapped) buffers and an even n.
+ *     operand over PCIe (A / S / U's upper and L's lower triangles, rows
+ *     rounded to 8-column tiles; X back the same way).  From n = 16 on the
+ *     copy engines move the contiguous mostly-needed half of the rows (one
+ *     strided copy per chunk) and zero-copy kernels, reading / writing the
+ *     mapped pinned host memory directly, only the remaining small triangle.
+ *     Needs pinned (cudaHostAlloc / cudaHostRegister-mapped) buffers and an
+ *     even n.
  *   LAGEN_HOST_X_ZEROED: the caller's X already holds zeros in its
  *     structurally-zero part (the reference's contract: "outputs must be
  *     zero-initialised by the caller", codegen.py:4-7); Cholesky then writes

@@ -18,7 +18,9 @@ struct PipeEntry {
 };
 
 // default mode per tile count
-constexpr int pipe_default_mode(int eq, int t) { return t <= 2 ? 1 : 0; }
+// solo (one warp per problem) for T <= 2, and for Sylvester T = 4 where it beats
+// both the split roles and the rowsweep engine (profiles/r02_pipe_solo.txt)
+constexpr int pipe_default_mode(int eq, int t) { return (t <= 2 || (eq == 2 && t == 4)) ? 1 : 0; }
 
 template <int EQ, int N, int MODE>
 cudaError_t launch_pipe_mode(const LaunchArgs& a, cudaStream_t s) {

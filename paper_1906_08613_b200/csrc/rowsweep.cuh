@@ -26,6 +26,10 @@
 
 #include "engine.cuh"
 
+#ifndef LAGEN_RSW_SYMK
+#define LAGEN_RSW_SYMK 1
+#endif
+
 namespace lagen {
 namespace rsw {
 
@@ -53,13 +57,14 @@ struct RCfg {
   static constexpr size_t SMEM = (size_t)W * PPW * PSZ * 8;
   // CTAs per SM and the substitution form, measured per (equation, n) over
   // MINB in 2..8 x {scaled, unscaled} at the BASELINE batches
-  // (tools/experiments/rsw_bench.cu, profiles/r02_rowsweep_sweep.txt): more
+  // (tools/experiments/rsw_bench.cu, profiles/r02_rowsweep_sweep.txt; Lyapunov
+  // re-swept with the symmetric shortcut, r02_rowsweep_symk.txt): more
   // CTAs hide the substitution chain's latency even where the row of y then
   // spills a few registers; the scaled form (a DFMA less on the chain, n - 1
   // more products live) wins where registers allow.  Index n / 4.
   static constexpr int mn(int a, int b) { return a < b ? a : b; }
-  static constexpr int kMinb[2][9] = {{0, 8, 8, 5, 4, 3, 5, 4, 3}, {0, 8, 8, 6, 5, 5, 5, 4, 4}};
-  static constexpr bool kScaled[2][9] = {{0, 0, 0, 1, 1, 1, 0, 0, 1}, {0, 0, 0, 1, 0, 0, 0, 0, 0}};
+  static constexpr int kMinb[2][9] = {{0, 8, 8, 5, 4, 4, 3, 3, 3}, {0, 8, 8, 6, 5, 5, 5, 4, 4}};
+  static constexpr bool kScaled[2][9] = {{0, 0, 0, 1, 1, 0, 1, 1, 0}, {0, 0, 0, 1, 0, 0, 0, 0, 0}};
   static constexpr int RMIN = N > 16 ? 168 : N > 8 ? 96 : 64;
   static constexpr int MINB_FIT = mn(mn((227 * 1024) / (int)SMEM, 2048 / THREADS), 65536 / (THREADS * RMIN));
   static constexpr int MINB0 = N % 4 == 0 ? mn(kMinb[EQ - 1][N / 4], mn((227 * 1024) / (int)SMEM, 2048 / THREADS)) : MINB_FIT;
@@ -136,18 +141,25 @@ __global__ void __launch_bounds__(RCfg<EQ, N>::THREADS, RCfg<EQ, N>::MINB)
       // l_rk piv_r is off the chain); otherwise DMUL -> SHFL -> DFMA on y
       // (fewer live registers: measured per size, RCfg::SCALED)
       double x;
+      // Lyapunov (SYMK): X is symmetric, so x_kc for k < c is already known
+      // as x_ck — lane c's finished y[k] — and its broadcast does not wait
+      // for this column's chain; only the steps k >= c are dependent
+      // (n^2 / 2 chained steps instead of n^2).
+      constexpr bool SYMK = EQ == 1 && LAGEN_RSW_SYMK;
       if constexpr (P::SCALED) {
         double z = y[c] * piv;
 #pragma unroll
         for (int k = 0; k < N - 1; ++k) {
-          const double xk = __shfl_sync(0xffffffffu, z, gbase + k);
+          const double xk = (SYMK && k < c) ? __shfl_sync(0xffffffffu, y[k], gbase + c)
+                                            : __shfl_sync(0xffffffffu, z, gbase + k);
           z = fma(-(lr[k] * piv), xk, z);
         }
         x = z;
       } else {
 #pragma unroll
         for (int k = 0; k < N - 1; ++k) {
-          const double xk = __shfl_sync(0xffffffffu, y[c] * piv, gbase + k);
+          const double xk = (SYMK && k < c) ? __shfl_sync(0xffffffffu, y[k], gbase + c)
+                                            : __shfl_sync(0xffffffffu, y[c] * piv, gbase + k);
           y[c] = fma(-lr[k], xk, y[c]);
         }
         x = y[c] * piv;

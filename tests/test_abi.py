@@ -158,3 +158,28 @@ def test_big_engine_size_range():
         assert not _lib.engine_supported(EQ_CODES[eq], big + 4, 4, 0, "generic")
         assert not _lib.engine_supported(EQ_CODES[eq], 256, 7, 0, "generic")
         assert not _lib.engine_supported(EQ_CODES[eq], 256, 8, 0, "warp")
+
+
+def test_host_bytes_of_the_hybrid_triangle_transfer():
+    """lagen_b200_host_bytes_flags counts what the host pipeline moves: with
+    LAGEN_HOST_TRIANGLES and n >= 16 the copy engines take rows [0, s) of an
+    upper part / rows [s, n) of a lower part at full width (s = n / 2 on the
+    8-column grid) and the zero-copy kernels the remaining triangle."""
+    from paper_1906_08613_b200 import executor
+    n, batch = 64, 10
+    s = 32
+    upper = s * n + sum(n - 8 * (r // 8) for r in range(s, n))
+    lower = (n - s) * n + sum(min(n, 8 * (r // 8) + 8) for r in range(s))
+    assert upper == 2688 and lower == 2688
+    h2d, d2h = _lib.host_bytes(EQ_CODES["cholesky"], n, batch, _lib.HOST_TRIANGLES | _lib.HOST_X_ZEROED)
+    assert h2d == batch * upper * 8 and d2h == batch * (upper * 8 + 4)
+    h2d, d2h = _lib.host_bytes(EQ_CODES["cholesky"], n, batch, _lib.HOST_TRIANGLES)
+    assert h2d == batch * upper * 8 and d2h == batch * (n * n * 8 + 4)      # X comes back dense unless zeroed by the caller
+    h2d, d2h = _lib.host_bytes(EQ_CODES["lyapunov"], n, batch, _lib.HOST_TRIANGLES)
+    assert h2d == batch * (lower + upper) * 8 and d2h == batch * (n * n * 8 + 4)
+    h2d, d2h = _lib.host_bytes(EQ_CODES["sylvester"], n, batch, _lib.HOST_TRIANGLES)
+    assert h2d == batch * (lower + upper + n * n) * 8
+    h2d, d2h = _lib.host_bytes(EQ_CODES["sylvester"], n, batch, 0)
+    assert h2d == batch * 3 * n * n * 8 and d2h == batch * (n * n * 8 + 4)
+    assert executor.host_triangles_default("cholesky", 16) and not executor.host_triangles_default("cholesky", 12)
+    assert not executor.host_triangles_default("sylvester", 132)
