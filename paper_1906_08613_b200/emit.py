@@ -30,6 +30,7 @@ import ctypes
 import hashlib
 import os
 import subprocess
+import threading
 from dataclasses import dataclass
 from pathlib import Path
 
@@ -146,9 +147,12 @@ def compile_module(mod, out_dir=None, force=False):
     so = out_dir / f"{mod.name}.{mod.digest}.so"
     if so.exists() and not force:
         return so
-    src = out_dir / f"{mod.name}.cu"
+    # per-process / per-thread scratch names: concurrent builds of the same
+    # module (two ranks, a thread pool) must not share intermediate files
+    uniq = f"{os.getpid()}_{threading.get_ident()}"
+    src = out_dir / f"{mod.name}.{mod.digest}.{uniq}.cu"
     src.write_text(mod.text)
-    tmp = so.with_suffix(".tmp")
+    tmp = out_dir / f"{mod.name}.{mod.digest}.{uniq}.tmp"
     # hidden visibility + no STB_GNU_UNIQUE: the module instantiates the same
     # templates as liblagen_b200.so (and as other emitted modules); their
     # function-local statics (per-kernel "configured" flags of launch_warp) and
@@ -161,6 +165,7 @@ def compile_module(mod, out_dir=None, force=False):
     if proc.returncode != 0:
         raise errors.LagenError(f"nvcc failed on the emitted kernel {mod.name}:\n{proc.stderr[-2000:]}")
     os.replace(tmp, so)
+    os.replace(src, out_dir / f"{mod.name}.cu")  # keep the last emitted source beside the module
     return so
 
 

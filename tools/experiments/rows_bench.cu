@@ -72,6 +72,15 @@ int main(int argc, char** argv) {
   CK(cudaGetLastError());
   const double byt = (12.0 * N * N + 4.0 * N) * batch;
   printf("time %.4f ms  GB/s = %.1f  roofline frac = %.3f\n", best, byt / best / 1e6, byt / 6553e9 * 1e3 / best);
+#ifdef LAGEN_ROWS_PROF
+  {
+    unsigned long long hp[16];
+    CK(cudaMemcpyFromSymbol(hp, lagen::cr::prof_buf, sizeof(hp)));
+    const double runs = 7.0;  // kernel launches above
+    printf("phase cycles per launch (CTA 0, group 0): leaf warp A=%.0f barrier=%.0f trsm=%.0f barrier=%.0f | panel warp A=%.0f barrier=%.0f trsm=%.0f barrier=%.0f\n",
+           hp[0] / runs, hp[1] / runs, hp[2] / runs, hp[3] / runs, hp[8] / runs, hp[9] / runs, hp[10] / runs, hp[11] / runs);
+  }
+#endif
   std::vector<long long> sample;
   for (long long p = 0; p < batch && p < 4; ++p) sample.push_back(p);
   for (long long p = batch > 4 ? batch - 4 : 0; p < batch; ++p) sample.push_back(p);
