@@ -98,6 +98,16 @@ struct PCfg {
   static constexpr int THREADS = PP * GW * 32;
   static constexpr size_t SMEM = (size_t)PP * SLOT * 8;
   static constexpr int mn(int a, int b) { return a < b ? a : b; }
+  // tile-solve formulation (sol_step): SOLVE2 keeps only FMA -> FMA -> MUL ->
+  // SHFL on the dependent chain and predicates the idle 8-lane groups' shared
+  // memory accesses off; measured faster only where one CTA per SM runs four
+  // solver warps (Sylvester T >= 13: 2-11 %), slower or neutral elsewhere
+  // (profiles/r02_pipe_solver_ab.txt)
+#ifdef LAGEN_PIPE_SOLVE2
+  static constexpr bool SOLVE2 = LAGEN_PIPE_SOLVE2 != 0;
+#else
+  static constexpr bool SOLVE2 = MODE == 0 && EQ == 2 && T >= 13;
+#endif
   // CTAs per SM for __launch_bounds__ (it sets the register budget).  Split
   // roles: measured per tile count over MINB = 1..8 at the BASELINE batches
   // (tools/experiments/pipe_bench.cu, profiles/r02_pipe_minb_sweep.txt) — more
@@ -412,106 +422,231 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
     const double* Ld = Lt + ltidx(I, I) * 64;
     const double* Ud = EQ == 2 ? Ut + utidx(J, J) * 64 : Lt + ltidx(J, J) * 64;
     auto uat = [&](int k) -> double { return EQ == 2 ? Ud[sw(k, c)] : Ud[sw(c, k)]; };
-    // uo[j] = U_JJ(j, c) for j <= c - 2 (older row values, from the scratch),
-    // u1 = U_JJ(c - 1, c) (newest, by shuffle); 0 elsewhere
-    double uo[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    double u1 = 0.0;
-    {
-      const double ucc = uat(c);
-      double dg[8];
+    if constexpr (!P::SOLVE2) {
+      // uo[j] = U_JJ(j, c) for j <= c - 2 (older row values, from the scratch),
+      // u1 = U_JJ(c - 1, c) (newest, by shuffle); 0 elsewhere
+      double uo[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      double u1 = 0.0;
+      {
+        const double ucc = uat(c);
+        double dg[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) dg[r] = Ld[sw(r, r)];
+        for (int r = 0; r < 8; ++r) dg[r] = Ld[sw(r, r)];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) scr[32 * r] = (8 * I + r < N && 8 * J + c < N) ? recip(dg[r] + ucc) : 0.0;
+        for (int r = 0; r < 8; ++r) scr[32 * r] = (8 * I + r < N && 8 * J + c < N) ? recip(dg[r] + ucc) : 0.0;
 #pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        const double v = uat(j);
-        uo[j] = j + 2 <= c ? v : 0.0;
+        for (int j = 0; j < 6; ++j) {
+          const double v = uat(j);
+          uo[j] = j + 2 <= c ? v : 0.0;
+        }
+        const double u1v = uat(c >= 1 ? c - 1 : 0);
+        u1 = c >= 1 ? u1v : 0.0;
       }
-      const double u1v = uat(c >= 1 ? c - 1 : 0);
-      u1 = c >= 1 ? u1v : 0.0;
-    }
-    if constexpr (MODE == 0) asm volatile("bar.sync 2, %0;" ::"n"(P::THREADS) : "memory");
-    else __syncwarp();
-    if (sv == 0) stamp(4 * (d + 1) + 1);
-    // solve: lane c owns column c; y / h: circular buffers of 8 over the
-    // steps (slot s & 7 = row s - c), static register indices.  The row
-    // contribution sum_{j<c} x_rj u_jc takes x_{r,c-1} (one step old) by
-    // shuffle and the older ones from the scratch row (written >= 2 steps ago)
-    double* Sl = Sq + (7 - c) * 10 + c;             // + 10 s: element (s - c, c)
-    const double* Sr = Sq + (7 - c) * 10;           // + 10 s: row s - c
-    // pivot of row s - c: scr[32 ((s - c) & 7)] (rows outside the tile wrap around; their x is masked)
-    const int pl0 = (8 - c) & 7;
-    auto pl = [&](int s) -> double { return scr[32 * ((pl0 + s) & 7)]; };
-    const double* Ll = Lsh + (7 + 8 * I - c) * 10;  // + 10 s: L_II column s - c
-    const int src1 = (lane & ~7) | (c >= 1 ? c - 1 : c);
-    // (letting the groups without a tile skip the solve — no instructions, no
-    // wavefronts — measured 5-17 % slower: the divergence costs more registers)
-    const unsigned lm = 0xffffffffu;
-    double y[8];
+      if constexpr (MODE == 0) asm volatile("bar.sync 2, %0;" ::"n"(P::THREADS) : "memory");
+      else __syncwarp();
+      if (sv == 0) stamp(4 * (d + 1) + 1);
+      // solve: lane c owns column c; y / h: circular buffers of 8 over the
+      // steps (slot s & 7 = row s - c), static register indices.  The row
+      // contribution sum_{j<c} x_rj u_jc takes x_{r,c-1} (one step old) by
+      // shuffle and the older ones from the scratch row (written >= 2 steps ago)
+      double* Sl = Sq + (7 - c) * 10 + c;             // + 10 s: element (s - c, c)
+      const double* Sr = Sq + (7 - c) * 10;           // + 10 s: row s - c
+      // pivot of row s - c: scr[32 ((s - c) & 7)] (rows outside the tile wrap around; their x is masked)
+      const int pl0 = (8 - c) & 7;
+      auto pl = [&](int s) -> double { return scr[32 * ((pl0 + s) & 7)]; };
+      const double* Ll = Lsh + (7 + 8 * I - c) * 10;  // + 10 s: L_II column s - c
+      const int src1 = (lane & ~7) | (c >= 1 ? c - 1 : c);
+      // (letting the groups without a tile skip the solve — no instructions, no
+      // wavefronts — measured 5-17 % slower: the divergence costs more registers)
+      const unsigned lm = 0xffffffffu;
+      double y[8];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) y[s] = Sl[10 * s];
-    // sum_{j <= c-2} x_rj u_jc of step s's row r = s - c, computed one step
-    // ahead from the scratch row (its entries were written >= 2 steps before
-    // step s, so visible after the previous step's __syncwarp)
-    auto rowsum = [&](int s) -> double {
-      const double2* rw = reinterpret_cast<const double2*>(Sr + 10 * s);
-      const double2 r0 = rw[0], r1 = rw[1], r2 = rw[2];  // (columns 6, 7 are never "older": j <= c - 2 <= 5)
-      double t0 = r0.x * uo[0];
-      double t1 = r0.y * uo[1];
-      t0 = fma(r1.x, uo[2], t0);
-      t1 = fma(r1.y, uo[3], t1);
-      t0 = fma(r2.x, uo[4], t0);
-      t1 = fma(r2.y, uo[5], t1);
-      return t0 + t1;
-    };
-    // Program order matters (in-order issue): each step first loads what the
-    // next one needs, then runs the dependent chain x(r, c-1) --shfl--> FMA
-    // -> MUL -> x, shuffles x on right away, and only then the pushes and
-    // the next row sum (whose loads have landed by then)
-    double x1 = 0.0;                       // x(r, c-1) of the current step, by shuffle
-    double pcur = pl(0);
-    double vpre = y[0] - rowsum(0);        // y - older row contributions of the current step
-    auto step = [&](int s, int u) {
-      const bool act = (unsigned)(s - c) < 8u;
-      // loads: this step's L_II column (push), the next step's row / pivot
-      const double2* lc = reinterpret_cast<const double2*>(Ll + 10 * s);
-      const double2 la = lc[0], lb = lc[1], lcc = lc[2], ld = lc[3];
-      const double2* rw = reinterpret_cast<const double2*>(Sr + 10 * (s + 1));
-      double2 r0, r1, r2;
-      double pnxt = 0.0, yref = 0.0;
-      if (s < 14) {
-        r0 = rw[0], r1 = rw[1], r2 = rw[2];
-        pnxt = pl(s + 1);
-      }
-      if (s + 8 <= 14) yref = Sl[10 * (s + 8)];
-      // the chain
-      const double v = fma(-x1, u1, vpre);
-      const double x = act ? v * pcur : 0.0;
-      x1 = __shfl_sync(lm, x, src1);
-      // push into the next row first (the next step's vpre), then the rest
-      y[(u + 1) & 7] = fma(-la.y, x, y[(u + 1) & 7]);
-      if (s < 14) {
+      for (int s = 0; s < 8; ++s) y[s] = Sl[10 * s];
+      // sum_{j <= c-2} x_rj u_jc of step s's row r = s - c, computed one step
+      // ahead from the scratch row (its entries were written >= 2 steps before
+      // step s, so visible after the previous step's __syncwarp)
+      auto rowsum = [&](int s) -> double {
+        const double2* rw = reinterpret_cast<const double2*>(Sr + 10 * s);
+        const double2 r0 = rw[0], r1 = rw[1], r2 = rw[2];  // (columns 6, 7 are never "older": j <= c - 2 <= 5)
         double t0 = r0.x * uo[0];
         double t1 = r0.y * uo[1];
         t0 = fma(r1.x, uo[2], t0);
         t1 = fma(r1.y, uo[3], t1);
         t0 = fma(r2.x, uo[4], t0);
         t1 = fma(r2.y, uo[5], t1);
-        vpre = y[(u + 1) & 7] - (t0 + t1);
-        pcur = pnxt;
+        return t0 + t1;
+      };
+      // Program order matters (in-order issue): each step first loads what the
+      // next one needs, then runs the dependent chain x(r, c-1) --shfl--> FMA
+      // -> MUL -> x, shuffles x on right away, and only then the pushes and
+      // the next row sum (whose loads have landed by then)
+      double x1 = 0.0;                       // x(r, c-1) of the current step, by shuffle
+      double pcur = pl(0);
+      double vpre = y[0] - rowsum(0);        // y - older row contributions of the current step
+      auto step = [&](int s, int u) {
+        const bool act = (unsigned)(s - c) < 8u;
+        // loads: this step's L_II column (push), the next step's row / pivot
+        const double2* lc = reinterpret_cast<const double2*>(Ll + 10 * s);
+        const double2 la = lc[0], lb = lc[1], lcc = lc[2], ld = lc[3];
+        const double2* rw = reinterpret_cast<const double2*>(Sr + 10 * (s + 1));
+        double2 r0, r1, r2;
+        double pnxt = 0.0, yref = 0.0;
+        if (s < 14) {
+          r0 = rw[0], r1 = rw[1], r2 = rw[2];
+          pnxt = pl(s + 1);
+        }
+        if (s + 8 <= 14) yref = Sl[10 * (s + 8)];
+        // the chain
+        const double v = fma(-x1, u1, vpre);
+        const double x = act ? v * pcur : 0.0;
+        x1 = __shfl_sync(lm, x, src1);
+        // push into the next row first (the next step's vpre), then the rest
+        y[(u + 1) & 7] = fma(-la.y, x, y[(u + 1) & 7]);
+        if (s < 14) {
+          double t0 = r0.x * uo[0];
+          double t1 = r0.y * uo[1];
+          t0 = fma(r1.x, uo[2], t0);
+          t1 = fma(r1.y, uo[3], t1);
+          t0 = fma(r2.x, uo[4], t0);
+          t1 = fma(r2.y, uo[5], t1);
+          vpre = y[(u + 1) & 7] - (t0 + t1);
+          pcur = pnxt;
+        }
+        Sl[10 * s] = x;  // in place (0 outside the tile)
+        const double coef[8] = {0.0, la.y, lb.x, lb.y, lcc.x, lcc.y, ld.x, ld.y};
+#pragma unroll
+        for (int e = 2; e < 8; ++e) y[(u + e) & 7] = fma(-coef[e], x, y[(u + e) & 7]);
+        if (s + 8 <= 14) y[u] = yref;
+        __syncwarp(lm);
+      };
+#pragma unroll
+      for (int u = 0; u < 8; ++u) step(u, u);
+#pragma unroll
+      for (int u = 0; u < 7; ++u) step(8 + u, u);
+    } else {
+      // uo[j] = U_JJ(j, c) for j <= c - 3 (older row values, from the scratch),
+      // u2 = U_JJ(c - 2, c) and u1 = U_JJ(c - 1, c) (the two newest row values,
+      // by shuffle); 0 elsewhere
+      double uo[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      double u1 = 0.0, u2 = 0.0;
+      {
+        const double ucc = uat(c);
+        double dg[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) dg[r] = Ld[sw(r, r)];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) scr[32 * r] = (8 * I + r < N && 8 * J + c < N) ? recip(dg[r] + ucc) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          const double v = uat(j);
+          uo[j] = j + 3 <= c ? v : 0.0;
+        }
+        const double u1v = uat(c >= 1 ? c - 1 : 0);
+        u1 = c >= 1 ? u1v : 0.0;
+        const double u2v = uat(c >= 2 ? c - 2 : 0);
+        u2 = c >= 2 ? u2v : 0.0;
       }
-      Sl[10 * s] = x;  // in place (0 outside the tile)
-      const double coef[8] = {0.0, la.y, lb.x, lb.y, lcc.x, lcc.y, ld.x, ld.y};
+      if constexpr (MODE == 0) asm volatile("bar.sync 2, %0;" ::"n"(P::THREADS) : "memory");
+      else __syncwarp();
+      if (sv == 0) stamp(4 * (d + 1) + 1);
+      // solve: lane c owns column c, step s finishes element (r, c), r = s - c.
+      //   x_rc = p_rc (y_rc - sum_{k<r} l_rk x_kc - sum_{j<c} x_rj u_jc)
+      // The dependent chain of a step is only
+      //   x_{r-1,c} --FMA--> t --(shuffled x_{r,c-1}) FMA--> v --MUL--> x_rc --SHFL-->
+      // everything else has at least one step of slack: the contributions of
+      // rows <= r-2 of the column are pushed into y[] (circular buffer of 8 over
+      // the steps, static register indices), x_{r,c-2} arrives by a second
+      // shuffle one step earlier, and x_{r,j}, j <= c-3, were written to the
+      // scratch row >= 2 steps before their load (visible after __syncwarp).
+      // Lanes outside the tile (r < 0 or r > 7) run on garbage that only reaches
+      // other lanes outside the tile; their x is stored and pushed as 0.
+      double* Sl = Sq + (7 - c) * 10 + c;             // + 10 s: element (s - c, c)
+      const double* Sr = Sq + (7 - c) * 10;           // + 10 s: row s - c
+      // pivot of row s - c: scr[32 ((s - c) & 7)] (rows outside the tile wrap around; their x is masked)
+      const int pl0 = (8 - c) & 7;
+      auto pl = [&](int s) -> double { return scr[32 * ((pl0 + s) & 7)]; };
+      const double* Ll = Lsh + (7 + 8 * I - c) * 10;  // + 10 s: L_II column s - c
+      const int src1 = (lane & ~7) | (c >= 1 ? c - 1 : c);
+      const int src2 = (lane & ~7) | (c >= 2 ? c - 2 : c);
+      const unsigned lm = 0xffffffffu;
+      double y[8];
 #pragma unroll
-      for (int e = 2; e < 8; ++e) y[(u + e) & 7] = fma(-coef[e], x, y[(u + e) & 7]);
-      if (s + 8 <= 14) y[u] = yref;
-      __syncwarp(lm);
-    };
+      for (int s = 0; s < 8; ++s) y[s] = live ? Sl[10 * s] : 0.0;
+      // sum_{j <= c-3} x_rj u_jc of the row of step s, from the scratch row
+      auto rowsum3 = [&](int s) -> double {
+        const double2* rw = reinterpret_cast<const double2*>(Sr + 10 * s);
+        double2 r0 = make_double2(0.0, 0.0), r1 = r0;
+        double r2 = 0.0;
+        if (live) {
+          r0 = rw[0], r1 = rw[1];
+          r2 = Sr[10 * s + 4];
+        }
+        double t0 = r0.x * uo[0];
+        double t1 = r0.y * uo[1];
+        t0 = fma(r1.x, uo[2], t0);
+        t1 = fma(r1.y, uo[3], t1);
+        t0 = fma(r2, uo[4], t0);
+        return t0 + t1;
+      };
+      double xu = 0.0;                 // this lane's previous element (unmasked)
+      double x1 = 0.0;                 // x(r, c-1) for the current step, by shuffle
+      double x2 = 0.0;                 // x(r+1, c-2) for the next step, by shuffle
+      double l1 = 0.0;                 // L_II(r, r-1)
+      double pcur = live ? pl(0) : 0.0;
+      double base = y[0] - rowsum3(0);
+      double rs3 = rowsum3(1);
+      double2 ca = make_double2(0.0, 0.0), cb = ca, cc = ca, cd = ca;  // L_II column r below the diagonal (this step's pushes)
+      if (live) {
+        const double2* lc = reinterpret_cast<const double2*>(Ll);
+        ca = lc[0], cb = lc[1], cc = lc[2], cd = lc[3];
+      }
+      double2 r0 = make_double2(0.0, 0.0), r1 = r0;  // scratch row of step s + 2
+      double r2 = 0.0;
+      auto step = [&](int s, int u) {
+        const bool act = (unsigned)(s - c) < 8u;
+        // loads for later steps: the scratch row of step s + 2 (its entries
+        // j <= c - 3 were stored before the previous step's __syncwarp)
+        if (s < 13 && live) {
+          const double2* rw = reinterpret_cast<const double2*>(Sr + 10 * (s + 2));
+          r0 = rw[0], r1 = rw[1];
+          r2 = Sr[10 * (s + 2) + 4];
+        }
+        // the chain
+        const double t = fma(-l1, xu, base);
+        const double v = fma(-u1, x1, t);
+        xu = v * pcur;
+        x1 = __shfl_sync(lm, xu, src1);
+        const double x = act ? xu : 0.0;
+        // next step's right-hand side, without the two newest contributions
+        base = (y[(u + 1) & 7] - rs3) - u2 * x2;
+        x2 = __shfl_sync(lm, x, src2);
+        if (live) Sl[10 * s] = x;  // in place (0 outside the tile)
+        l1 = ca.y;
+        // pushes into rows r+2 .. r+7 of the column
+        const double coef[8] = {0.0, ca.y, cb.x, cb.y, cc.x, cc.y, cd.x, cd.y};
 #pragma unroll
-    for (int u = 0; u < 8; ++u) step(u, u);
+        for (int e = 2; e < 8; ++e) y[(u + e) & 7] = fma(-coef[e], x, y[(u + e) & 7]);
+        if (s + 8 <= 14 && live) y[u] = Sl[10 * (s + 8)];
+        if (s < 14 && live) {
+          pcur = pl(s + 1);
+          const double2* lc = reinterpret_cast<const double2*>(Ll + 10 * (s + 1));
+          ca = lc[0], cb = lc[1], cc = lc[2], cd = lc[3];
+        }
+        if (s < 13) {
+          double t0 = r0.x * uo[0];
+          double t1 = r0.y * uo[1];
+          t0 = fma(r1.x, uo[2], t0);
+          t1 = fma(r1.y, uo[3], t1);
+          t0 = fma(r2, uo[4], t0);
+          rs3 = t0 + t1;
+        }
+        __syncwarp(lm);
+      };
 #pragma unroll
-    for (int u = 0; u < 7; ++u) step(8 + u, u);
+      for (int u = 0; u < 8; ++u) step(u, u);
+#pragma unroll
+      for (int u = 0; u < 7; ++u) step(8 + u, u);
+    }
     if (sv == 0) stamp(4 * (d + 1) + 2);
     // column c of X (Lyapunov diagonal tile: lower := mirror of upper) ->
     // the published tile as -X (swizzled), and X -> HBM
