@@ -79,7 +79,17 @@ struct PCfg {
   static constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
   // tiles on the longest anti-diagonal (Lyapunov: upper tiles only)
   static constexpr int MAXM = EQ == 2 ? T : cdiv(T, 2);
-  static constexpr int CU = MODE == 1 ? T : (EQ == 2 ? (T >= 13 ? 1 : 2) : 2);  // columns per updater warp
+  // columns per updater warp: pairs (boustrophedon / folded) while several
+  // CTAs share an SM; one column per warp where one CTA per SM runs (more
+  // warps per problem; Sylvester T = 11, 12: 8-14 % with SOLVE2, Lyapunov
+  // T >= 14: 1-11 %, profiles/r02_pipe_solver_ab.txt)
+#ifndef LAGEN_PIPE_SYLV_CU1_T
+#define LAGEN_PIPE_SYLV_CU1_T 11
+#endif
+#ifndef LAGEN_PIPE_LYAP_CU1_T
+#define LAGEN_PIPE_LYAP_CU1_T 14
+#endif
+  static constexpr int CU = MODE == 1 ? T : (EQ == 2 ? (T >= LAGEN_PIPE_SYLV_CU1_T ? 1 : 2) : (T >= LAGEN_PIPE_LYAP_CU1_T ? 1 : 2));
   static constexpr int NU = MODE == 1 ? 1 : cdiv(T, CU);
   static constexpr int NS = MODE == 1 ? 0 : cdiv(MAXM, 4);
   static_assert(MODE == 0 || MAXM <= 4, "solo mode: one warp solves at most 4 tiles per step");
@@ -100,13 +110,13 @@ struct PCfg {
   static constexpr int mn(int a, int b) { return a < b ? a : b; }
   // tile-solve formulation (sol_step): SOLVE2 keeps only FMA -> FMA -> MUL ->
   // SHFL on the dependent chain and predicates the idle 8-lane groups' shared
-  // memory accesses off; measured faster only where one CTA per SM runs four
-  // solver warps (Sylvester T >= 13: 2-11 %), slower or neutral elsewhere
-  // (profiles/r02_pipe_solver_ab.txt)
+  // memory accesses off; measured faster only where one CTA per SM runs with
+  // one column per updater warp (Sylvester T >= 11: 2-14 %, Lyapunov T = 14,
+  // 15: 2-5 %), slower or neutral elsewhere (profiles/r02_pipe_solver_ab.txt)
 #ifdef LAGEN_PIPE_SOLVE2
   static constexpr bool SOLVE2 = LAGEN_PIPE_SOLVE2 != 0;
 #else
-  static constexpr bool SOLVE2 = MODE == 0 && EQ == 2 && T >= 13;
+  static constexpr bool SOLVE2 = MODE == 0 && (EQ == 2 ? T >= LAGEN_PIPE_SYLV_CU1_T : (T == 14 || T == 15));
 #endif
   // CTAs per SM for __launch_bounds__ (it sets the register budget).  Split
   // roles: measured per tile count over MINB = 1..8 at the BASELINE batches
@@ -117,7 +127,7 @@ struct PCfg {
   static constexpr int RMIN = MODE == 1 ? 128 : 96;
   static constexpr int fitb(int b) { return (b <= 1 || 65536 / (THREADS * b) >= RMIN) ? b : fitb(b - 1); }
   static constexpr int MINB_FIT = fitb(mn(smem_fit(PP), 2048 / THREADS));
-  static constexpr int kLyapMinb[17] = {1, 1, 1, 1, 7, 7, 6, 4, 4, 3, 2, 2, 2, 2, 2, 1, 1};
+  static constexpr int kLyapMinb[17] = {1, 1, 1, 1, 7, 7, 6, 4, 4, 3, 2, 2, 2, 2, 1, 1, 1};
   static constexpr int kSylvMinb[17] = {1, 1, 1, 1, 4, 4, 4, 3, 2, 2, 2, 1, 1, 1, 1, 1, 1};
   static constexpr int MINB_TAB = mn(EQ == 1 ? kLyapMinb[T] : kSylvMinb[T], mn(smem_fit(PP), 2048 / THREADS));
   static constexpr int MINB0 = (MODE == 1 || T < 4) ? MINB_FIT : MINB_TAB;
