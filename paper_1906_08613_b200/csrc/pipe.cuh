@@ -113,6 +113,28 @@ struct PCfg {
   // memory accesses off; measured faster only where one CTA per SM runs with
   // one column per updater warp (Sylvester T >= 11: 2-14 %, Lyapunov T = 14,
   // 15: 2-5 %), slower or neutral elsewhere (profiles/r02_pipe_solver_ab.txt)
+  // first solve formulation: shared-memory accesses of the 8-lane groups
+  // without a tile predicated off.  The solve is bound by the SM's shared
+  // memory / shuffle pipe (about 45 cycles of it per element step and solver
+  // warp: 7 LDS.128, 3 LDS.64, STS.64, a 64-bit SHFL at 8.6), so the idle
+  // groups' loads cost as much as the live ones'; the predicates cost a few
+  // registers, so it is on where measured faster (profiles/r02_pipe_solver_ab.txt)
+  static constexpr bool pred_on() {
+    if (MODE == 1) return false;
+    if (EQ == 2) return T >= 5 && T <= 8;
+    return N == 52 || N == 56 || N == 60 || N == 64 || N == 72 || N == 76 || N == 80 || N == 84 || N == 100 || N == 124 ||
+           N == 128;
+  }
+#ifdef LAGEN_PIPE_PRED
+  static constexpr bool PRED = LAGEN_PIPE_PRED != 0;
+#else
+  static constexpr bool PRED = pred_on();
+#endif
+#ifdef LAGEN_PIPE_PRED_SETUP
+  static constexpr bool PRED_SETUP = LAGEN_PIPE_PRED_SETUP != 0;
+#else
+  static constexpr bool PRED_SETUP = false;
+#endif
 #ifdef LAGEN_PIPE_SOLVE2
   static constexpr bool SOLVE2 = LAGEN_PIPE_SOLVE2 != 0;
 #else
@@ -437,7 +459,7 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
       // u1 = U_JJ(c - 1, c) (newest, by shuffle); 0 elsewhere
       double uo[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       double u1 = 0.0;
-      {
+      if (live || !P::PRED_SETUP) {
         const double ucc = uat(c);
         double dg[8];
 #pragma unroll
@@ -469,15 +491,17 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
       // (letting the groups without a tile skip the solve — no instructions, no
       // wavefronts — measured 5-17 % slower: the divergence costs more registers)
       const unsigned lm = 0xffffffffu;
+      const bool lv = live || !P::PRED;  // groups without a tile: no shared-memory traffic
       double y[8];
 #pragma unroll
-      for (int s = 0; s < 8; ++s) y[s] = Sl[10 * s];
+      for (int s = 0; s < 8; ++s) y[s] = lv ? Sl[10 * s] : 0.0;
       // sum_{j <= c-2} x_rj u_jc of step s's row r = s - c, computed one step
       // ahead from the scratch row (its entries were written >= 2 steps before
       // step s, so visible after the previous step's __syncwarp)
       auto rowsum = [&](int s) -> double {
         const double2* rw = reinterpret_cast<const double2*>(Sr + 10 * s);
-        const double2 r0 = rw[0], r1 = rw[1], r2 = rw[2];  // (columns 6, 7 are never "older": j <= c - 2 <= 5)
+        double2 r0 = make_double2(0.0, 0.0), r1 = r0, r2 = r0;
+        if (lv) r0 = rw[0], r1 = rw[1], r2 = rw[2];  // (columns 6, 7 are never "older": j <= c - 2 <= 5)
         double t0 = r0.x * uo[0];
         double t1 = r0.y * uo[1];
         t0 = fma(r1.x, uo[2], t0);
@@ -491,21 +515,22 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
       // -> MUL -> x, shuffles x on right away, and only then the pushes and
       // the next row sum (whose loads have landed by then)
       double x1 = 0.0;                       // x(r, c-1) of the current step, by shuffle
-      double pcur = pl(0);
+      double pcur = lv ? pl(0) : 0.0;
       double vpre = y[0] - rowsum(0);        // y - older row contributions of the current step
+      // (loaded values persist in the idle groups: predicated loads, no re-zeroing)
+      double2 la = make_double2(0.0, 0.0), lb = la, lcc = la, ld = la, r0 = la, r1 = la, r2 = la;
+      double pnxt = 0.0, yref = 0.0;
       auto step = [&](int s, int u) {
         const bool act = (unsigned)(s - c) < 8u;
         // loads: this step's L_II column (push), the next step's row / pivot
         const double2* lc = reinterpret_cast<const double2*>(Ll + 10 * s);
-        const double2 la = lc[0], lb = lc[1], lcc = lc[2], ld = lc[3];
+        if (lv) la = lc[0], lb = lc[1], lcc = lc[2], ld = lc[3];
         const double2* rw = reinterpret_cast<const double2*>(Sr + 10 * (s + 1));
-        double2 r0, r1, r2;
-        double pnxt = 0.0, yref = 0.0;
-        if (s < 14) {
+        if (s < 14 && lv) {
           r0 = rw[0], r1 = rw[1], r2 = rw[2];
           pnxt = pl(s + 1);
         }
-        if (s + 8 <= 14) yref = Sl[10 * (s + 8)];
+        if (s + 8 <= 14 && lv) yref = Sl[10 * (s + 8)];
         // the chain
         const double v = fma(-x1, u1, vpre);
         const double x = act ? v * pcur : 0.0;
@@ -522,7 +547,7 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
           vpre = y[(u + 1) & 7] - (t0 + t1);
           pcur = pnxt;
         }
-        Sl[10 * s] = x;  // in place (0 outside the tile)
+        if (lv) Sl[10 * s] = x;  // in place (0 outside the tile)
         const double coef[8] = {0.0, la.y, lb.x, lb.y, lcc.x, lcc.y, ld.x, ld.y};
 #pragma unroll
         for (int e = 2; e < 8; ++e) y[(u + e) & 7] = fma(-coef[e], x, y[(u + e) & 7]);
