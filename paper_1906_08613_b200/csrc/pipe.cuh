@@ -165,6 +165,7 @@ struct PCfg {
 // padded X entries ever read them
 template <int N, int T, int PART, int G>
 __device__ __forceinline__ void load_tri(double* tiles, const double* __restrict__ src, int rank) {
+#ifdef LAGEN_PIPE_LOAD_ROWMAJOR
   constexpr int NP = 8 * T, HP = NP / 2;
   for (int u = rank; u < NP * HP; u += G) {
     const int r = u / HP, cp = u - r * HP;
@@ -178,6 +179,35 @@ __device__ __forceinline__ void load_tri(double* tiles, const double* __restrict
       *reinterpret_cast<double2*>(dst) = make_double2(r == c ? 1.0 : 0.0, r == c + 1 ? 1.0 : 0.0);
     }
   }
+#else
+  // a warp per tile and pass: lane (r8, p) moves the 16-byte pair (r8, 2 p) of
+  // tile t; the tiles are walked in storage order (t = ltidx / utidx), the
+  // tile coordinates follow incrementally — no division and no iterations over
+  // the other triangle
+  constexpr int NWG = G / 32, NT = T * (T + 1) / 2;
+  const int wq = rank >> 5, lane = rank & 31;
+  const int r8 = lane >> 2, c2 = 2 * (lane & 3);
+  const int so = sw(r8, c2);
+  int a = 0, bq = wq;  // tile t = a (a + 1) / 2 + bq, bq <= a: (I, J) = (a, bq) lower, (bq, a) upper
+  while (bq > a) {
+    bq -= a + 1;
+    ++a;
+  }
+  for (int t = wq; t < NT; t += NWG) {
+    const int r = 8 * (PART == 0 ? a : bq) + r8, c = 8 * (PART == 0 ? bq : a) + c2;
+    double* dst = tiles + t * 64 + so;
+    if (r < N && c < N) {  // N even: the pair is inside
+      cp_async16(dst, src + r * N + c);
+    } else {
+      *reinterpret_cast<double2*>(dst) = make_double2(r == c ? 1.0 : 0.0, r == c + 1 ? 1.0 : 0.0);
+    }
+    bq += NWG;
+    while (bq > a) {
+      bq -= a + 1;
+      ++a;
+    }
+  }
+#endif
 }
 
 template <int EQ, int N, int MODE>
@@ -219,10 +249,17 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
   // profiling (tools/pipe_profile.py): clock64 per phase of the first
   // problem of CTA 0, solver warp 0 -> prof[4 (d + 1) + k], updater warp 0 ->
   // prof[256 + 2 (d + 1) + k]
+  // (compiled in with -DLAGEN_PIPE_PROF only: the tests cost ~4 % of the
+  // kernel's instructions; tools/experiments/pipe_build.sh defines it)
+#ifdef LAGEN_PIPE_PROF
   unsigned long long* pr = nullptr;
   auto stamp = [&](int idx) {
     if (pr && lane == 0) pr[idx] = clock64();
   };
+#else
+  (void)prof;
+  auto stamp = [&](int) {};
+#endif
   auto i0of = [&](int dd) { return dd - T + 1 > 0 ? dd - T + 1 : 0; };
   // published -X of diagonal dd: buffer dd mod 2, tile (I, dd - I) at row
   // I - i0(dd) (the base is shifted so that row I is base + I * PS)
@@ -757,7 +794,9 @@ __global__ void __launch_bounds__(PCfg<EQ, N, MODE>::THREADS, PCfg<EQ, N, MODE>:
     cp_async_commit();
     if (rank == 0) *flag = 0;
     bool bad = false;
+#ifdef LAGEN_PIPE_PROF
     pr = (prof && blockIdx.x == 0 && prob == grp * gridDim.x) ? prof : nullptr;
+#endif
     // the roles run separate step loops with the same barrier sequence, so
     // the accumulators are live only in the updater warps' registers
     if (MODE == 1 || is_upd) {

@@ -105,8 +105,11 @@ int main(int argc, char** argv) {
       if (u[0] && u[1]) su += u[1] - u[0];
     }
     const unsigned long long* s0 = hp + 4, *sl = hp + 4 * (2 * T - 1);
-    printf("steps=%d per step: wait=%.0f solve=%.0f out=%.0f | upd=%.0f | problem=%.0f cycles\n", 2 * T - 1, sw / cnt, ss / cnt,
-           so / cnt, su / (2 * T - 1), (double)(sl[3] - s0[0]));
+    if (cnt)
+      printf("steps=%d per step: wait=%.0f solve=%.0f out=%.0f | upd=%.0f | problem=%.0f cycles\n", 2 * T - 1, sw / cnt, ss / cnt,
+             so / cnt, su / (2 * T - 1), (double)(sl[3] - s0[0]));
+    else
+      printf("steps=%d (no per-step clocks: built without LAGEN_PIPE_PROF)\n", 2 * T - 1);
   }
   // residual of a sample
   std::vector<long long> sample;
