@@ -111,6 +111,17 @@ struct KRow {
   }
 };
 
+// packed offsets of the first stored element of rows r0 .. r0 + B - 1 (r0 a
+// multiple of 4): one Rows::off and an add per row instead of B closed forms
+// (the per-block-row offsets were ~10 % of the kernel's instructions)
+template <int N, int B>
+__device__ __forceinline__ void row_starts(int r0, int (&o)[B]) {
+  const int w0 = N - r0;  // stored length of rows r0 .. r0 + 3
+  const int b0 = Rows<N>::off(r0);
+#pragma unroll
+  for (int i = 0; i < B; ++i) o[i] = i < 4 ? b0 + i * w0 : b0 + 4 * w0 + (i - 4) * (w0 - 4);
+}
+
 // row-major n x n (upper part) -> packed rows, cp.async 16-byte units; full
 // rows are walked (division by the compile-time half-width) and the chunks
 // left of each row's first stored column are skipped
@@ -316,10 +327,12 @@ template <int N, int B>
 __device__ __forceinline__ void leaf(double* xs, int r0, double* rsb, int* flag) {
   const int lane = lane_id();
   double t[B][B];
+  int os[B];
+  row_starts<N, B>(r0, os);
 #pragma unroll
   for (int r = 0; r < B; ++r) {
     // row r0 + r is stored from column 4 * floor((r0 + r) / 4) = r0 + (r & ~3)
-    const int o = Rows<N>::at(r0 + r, r0 + (r & ~3));
+    const int o = os[r];
 #pragma unroll
     for (int c = 0; c < B; c += 2) {
       if (c < (r & ~3)) {
@@ -382,8 +395,9 @@ __device__ __forceinline__ void leaf(double* xs, int r0, double* rsb, int* flag)
 template <int N, int B>
 __device__ __forceinline__ void trsm(double* xs, int r0, const double* rsb, int rank, int nthr) {
   int o[B];
+  row_starts<N, B>(r0, o);
 #pragma unroll
-  for (int i = 0; i < B; ++i) o[i] = Rows<N>::at(r0 + i, 0);
+  for (int i = 0; i < B; ++i) o[i] -= r0 + (i & ~3);  // -> element (r0 + i, c) at o[i] + c
   for (int c = r0 + B + rank; c < N; c += nthr) {
     double w[B];
 #pragma unroll
