@@ -44,6 +44,11 @@
 #ifndef LAGEN_ROWS_ROWLOOP_H
 #define LAGEN_ROWS_ROWLOOP_H 54
 #endif
+// the store's row walk got cheaper in round 2 (row start by an add, unrolled
+// passes): it now also wins at n = 68..104
+#ifndef LAGEN_ROWS_STORE_ROWLOOP_H
+#define LAGEN_ROWS_STORE_ROWLOOP_H 34
+#endif
 #ifndef LAGEN_ROWS_DBMIN
 #define LAGEN_ROWS_DBMIN 1000  // double-buffer when >= this many slots fit twice (off)
 #endif
@@ -421,16 +426,23 @@ __device__ __forceinline__ void store_rows(double* __restrict__ dst, const doubl
   // warps over the block row's rows, lanes over 16-byte pairs (coalesced)
   const int nb = r0 + bsz <= NR ? bsz : NR - r0;  // real rows of this block row
   constexpr int H = NR / 2;
-  if constexpr (H <= 32 || H % 32 == 0 || H >= LAGEN_ROWS_ROWLOOP_H) {
+  if constexpr (H <= 32 || H % 32 == 0 || H >= LAGEN_ROWS_STORE_ROWLOOP_H) {
     const int w = rank >> 5, nw = nthr >> 5, lane = rank & 31;
+    // r0 is a multiple of 4: row r0 + i starts at off(r0) + i (N - r0) - 4 max(i - 4, 0)
+    const int b0 = Rows<N>::off(r0), w0 = N - r0;
     for (int i = w; i < nb; i += nw) {
-      const int r = r0 + i, c0 = 4 * (r >> 2);
-      const double* row = xs + Rows<N>::off(r) - c0;
+      const int r = r0 + i, c0 = r0 + (i & ~3);
+      const int i4 = i > 4 ? i - 4 : 0;
+      const double* row = xs + b0 + i * w0 - 4 * i4 - c0;
       double* drow = dst + r * NR;
-      for (int c = 2 * lane; c < NR; c += 64) {
-        double2 v = make_double2(0.0, 0.0);
-        if (c >= c0) v = *reinterpret_cast<const double2*>(row + c);
-        __stcs(reinterpret_cast<double2*>(drow + c), v);
+#pragma unroll
+      for (int k = 0; k < (NR + 63) / 64; ++k) {
+        const int c = 2 * lane + 64 * k;
+        if (64 * k + 64 <= NR || c < NR) {
+          double2 v = make_double2(0.0, 0.0);
+          if (c >= c0) v = *reinterpret_cast<const double2*>(row + c);
+          __stcs(reinterpret_cast<double2*>(drow + c), v);
+        }
       }
     }
   } else {
