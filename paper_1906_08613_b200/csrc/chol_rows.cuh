@@ -426,7 +426,7 @@ __device__ __forceinline__ void store_rows(double* __restrict__ dst, const doubl
   // warps over the block row's rows, lanes over 16-byte pairs (coalesced)
   const int nb = r0 + bsz <= NR ? bsz : NR - r0;  // real rows of this block row
   constexpr int H = NR / 2;
-  if constexpr (H <= 32 || H % 32 == 0 || H >= LAGEN_ROWS_STORE_ROWLOOP_H) {
+  if constexpr (H <= 32 || H % 32 == 0 || (H >= LAGEN_ROWS_STORE_ROWLOOP_H && H != 42 && H != 36)) {  // (n = 72, 84 measured slower)
     const int w = rank >> 5, nw = nthr >> 5, lane = rank & 31;
     // r0 is a multiple of 4: row r0 + i starts at off(r0) + i (N - r0) - 4 max(i - 4, 0)
     const int b0 = Rows<N>::off(r0), w0 = N - r0;
