@@ -30,6 +30,20 @@
 namespace lagen {
 namespace col {
 
+// 1 / sqrt(a) for the Cholesky pivots: rsqrt.approx (MUFU.RSQ64H, ~2^-20)
+// and two Newton steps y <- y + y (1/2 - (a/2) y^2), 9 instructions instead
+// of the ~19 of rsqrt() with its special-case path (see chol_rows.cuh); <= 2 ulp for normal a > 0 — a <= 0, NaN and Inf
+// pivots are flagged by the callers before the value is used
+__device__ __forceinline__ double rsqrt_nr(double a) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  const double h = 0.5 * a;
+  double e = fma(-h, y * y, 0.5);
+  y = fma(y, e, y);
+  e = fma(-h, y * y, 0.5);
+  return fma(y, e, y);
+}
+
 template <int N>
 struct ColPolicy {
   static constexpr int W = N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : 32;  // lanes per problem
@@ -212,7 +226,7 @@ __global__ void __launch_bounds__(ColPolicy<N>::WARPS * 32, ColPolicy<N>::MINB)
           constexpr int i = decltype(iI)::value;
           const double piv = K::template bcast<i, i>(cs, gmask);
           if (gl == 0 && piv <= 0.0 && flag == 0) flag = i + 1;
-          const double rs = rsqrt(piv);
+          const double rs = N <= 16 ? rsqrt_nr(piv) : rsqrt(piv);  // (n >= 20 measured slower with the lean form)
           sfor<0, CPL>([&](auto sI) {
             constexpr int s = decltype(sI)::value;
             if constexpr (s == 1 || i < 32) {
@@ -279,7 +293,7 @@ __global__ void __launch_bounds__(ColPolicy<N>::WARPS * 32, ColPolicy<N>::MINB)
           constexpr int i = decltype(iI)::value;
           const double piv = t[i][i];
           if (gl == 0 && piv <= 0.0 && flag == 0) flag = s1 + i + 1;
-          rs[i] = rsqrt(piv);
+          rs[i] = N <= 16 ? rsqrt_nr(piv) : rsqrt(piv);
           t[i][i] = piv * rs[i];
           sfor<i + 1, B>([&](auto cI) {
             constexpr int c = decltype(cI)::value;
