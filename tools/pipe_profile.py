@@ -3,6 +3,14 @@ problem): solver warp 0 (start, after the critical DMMAs, after the solve,
 after the write-out) and updater warp 0 (start, end) per anti-diagonal step.
 
     python tools/pipe_profile.py --eq sylvester --n 128
+
+The stamps are compiled out of the default library (they cost ~4 % of the
+kernel's instructions); build it with them first:
+
+    LAGEN_NVCC_EXTRA=-DLAGEN_PIPE_PROF=1 python -m paper_1906_08613_b200.build --force
+
+(or use tools/experiments/pipe_bench.cu, which tools/experiments/pipe_build.sh
+builds with the stamps).
 """
 import argparse
 import ctypes
