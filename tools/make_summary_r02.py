@@ -55,7 +55,8 @@ def main():
            "`r02_ncu_launches_chol_sweep.csv` (ncu launch lists: time and DRAM bytes per launch of one step of each sweep), "
            "`r02_ncu_full_top_kernels.csv` (`ncu --set full` of the top kernels), `r02_traffic.json` (DRAM bytes vs "
            "algorithmic bytes), A/B and tuning records: `r02_pipe_solver_ab.txt` (tile-solve formulations, columns per "
-           "updater warp, predication, single-warp issue rates), `r02_rowsmix_ab.txt`, `r02_rowsmix_tune.txt`, "
+           "updater warp, predication, single-warp issue rates), `r02_ncu_pipe_solver_stalls.txt` (stall reasons inside the tile solve), "
+           "`r02_rows_trim.txt` (rows / column engine instruction trimming), `r02_rowsmix_ab.txt`, `r02_rowsmix_tune.txt`, "
            "`r02_pipe_minb_sweep.txt`, `r02_pipe_minb_resweep.txt`, `r02_pipe_lsu_fix.txt`, `r02_pipe_solo.txt`, "
            "`r02_rowsweep_sweep.txt`, `r02_rowsweep_symk.txt`, `r02_e2e_hybrid.txt`, `r02_e2e_nosplit.txt`, "
            "`r02_ncu_rows128_smem_lines.txt`, `r02_ncu_pipe_sylv64_smem_lines_before.txt`, `r02_chol_gang_experiment.md` "
